@@ -1,0 +1,174 @@
+/*
+ * include/dash.h -- C ABI of libdash.so: DASH deterministic attention
+ * backward for NVIDIA B200 (sm_100a).
+ *
+ * Paper: "DASH: Deterministic Attention Scheduling for High-Throughput
+ * Reproducible LLM Training", arXiv 2601.21824.  "P:n" below is line n of
+ * that paper's text; "AMB-k" is reading k of DESIGN.md §Readings.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Tensors q, k, v, o, dO, dq, dk, dv: bf16, layout [B, N, H, d], dense
+ *    row-major (d fastest), 16-byte aligned.  lse: fp32 [B, H, N],
+ *    natural-log logsumexp of the scaled scores (AMB-15).  These are
+ *    Algorithm 1's "Q, K, V, O, dO in R^{N x d}, logsumexp L in R^N"
+ *    for every (batch, head).
+ *  - Supported: d in {64, 128}; N a positive multiple of 128 (the KV/Q tile
+ *    size B_r = B_c = 128 of the schedule model, AMB-11); seqlen_q = seqlen_k.
+ *  - softmax_scale <= 0 selects 1/sqrt(d) (AMB-1).
+ *  - Device pointers are CUDA device pointers owned by the caller.  The
+ *    library never allocates device memory; all scratch lives in the
+ *    caller-provided workspace.  `stream` is a cudaStream_t (NULL = legacy
+ *    default stream); every call is stream-ordered and asynchronous unless
+ *    stated otherwise.  A workspace must not be used by two in-flight calls.
+ *  - Errors are returned as dash_status; nothing is thrown across the ABI.
+ *    DASH_ERR_INVALID_ARG: null pointer, misalignment, unsupported shape.
+ *    DASH_ERR_UNSUPPORTED: a legal request this build cannot run (see each
+ *    call).  DASH_ERR_WORKSPACE: workspace too small.  DASH_ERR_CUDA: a CUDA
+ *    runtime error (cudaGetLastError after launch).  DASH_ERR_DEADLOCK: a
+ *    ticket wait exceeded its bound in an earlier call on this workspace
+ *    (reported by the next call that synchronises, see dash_check_workspace).
+ */
+#ifndef DASH_H_
+#define DASH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DASH_OK = 0,
+  DASH_ERR_INVALID_ARG = 1,
+  DASH_ERR_UNSUPPORTED = 2,
+  DASH_ERR_WORKSPACE = 3,
+  DASH_ERR_CUDA = 4,
+  DASH_ERR_DEADLOCK = 5
+} dash_status;
+
+typedef enum { DASH_MASK_FULL = 0, DASH_MASK_CAUSAL = 1 } dash_mask;
+
+/* Q-tile visiting orders over the ordered dQ reduction (§3):
+ *  NAIVE      -- ascending Q tiles, dQ reduced in ascending KV order; the
+ *                FlashAttention-3 deterministic baseline.
+ *  DESCENDING -- Descending Q-Tile Iteration, same reduction order (§3.3,
+ *                P:91-103; AMB-6).
+ *  SHIFT      -- Shift Scheduling: cyclic shift for the full mask,
+ *                Symmetric Shift (KV pairs i, n-1-i, two phases) for the
+ *                causal mask; dQ reduced in visit-step order. */
+typedef enum {
+  DASH_SCHED_NAIVE = 0,
+  DASH_SCHED_DESCENDING = 1,
+  DASH_SCHED_SHIFT = 2
+} dash_schedule;
+
+typedef struct {
+  int batch;           /* B */
+  int seqlen;          /* N (= seqlen_q = seqlen_k) */
+  int heads;           /* H */
+  int head_dim;        /* d */
+  float softmax_scale; /* <= 0 -> 1/sqrt(d) */
+} dash_shape;
+
+/* Attention forward: o = softmax(scale * q k^T [+ causal mask]) v and the
+ * natural-log logsumexp lse, i.e. the O and L that Algorithm 1 requires
+ * (P:353).  Causal: key c is visible to query r iff c <= r.  Not the timed
+ * path; numerically an fp32-accumulating kernel with bf16 output.
+ * Returns DASH_ERR_INVALID_ARG / DASH_ERR_CUDA as described above. */
+dash_status dash_attn_fwd(const dash_shape* shape, const void* q, const void* k, const void* v,
+                          void* o, float* lse, int causal, void* stream);
+
+/* Bytes of device workspace dash_attn_bwd needs for this problem: the fp32
+ * dQ accumulator [B,H,N,d] (Alg.1 line 34's "dQ_i in global memory"),
+ * D = rowsum(dO o O) fp32 [B,H,N] (Alg.1 line 1; AMB-2), one int32
+ * ticket per (b, h, Q sub-tile) (the "global order"), the job
+ * counter and the schedule table.  Returns 0 for an invalid shape. */
+size_t dash_attn_bwd_workspace_bytes(const dash_shape* shape, int causal, int schedule,
+                                     int deterministic);
+
+/* Attention backward (Algorithm 1).  Computes
+ *   D = rowsum(dO o O); P = exp(scale*S - L); dS = P o (dP - D)
+ *   dV = P^T dO;  dK = scale * dS^T Q;  dQ = scale * dS K
+ * with each CTA owning a KV tile (dK, dV reduced on chip) and the dQ
+ * partials of all KV tiles added into an fp32 accumulator.
+ *  deterministic != 0: the adds into each dQ tile happen in the fixed order
+ *    of `schedule`, enforced by a per-Q-tile ticket (acquire/release), so
+ *    results are bitwise identical run to run and across (b, h) sharding.
+ *  deterministic == 0: the atomic comparison variant (Fig.1) -- the
+ *    same kernel with unordered reduce-adds; Q order still follows `schedule`.
+ * dq, dk, dv are written (not accumulated).  o and lse must come from the
+ * forward of the same inputs (dash_attn_fwd or any exact equivalent).
+ * DASH_ERR_UNSUPPORTED: SHIFT with causal and an odd number of KV tiles
+ * (AMB-10), or SHIFT needing more co-resident CTAs than the device holds
+ * (n_kv for full, n_kv/2 for causal; App. B of SURVEY.md, AMB-12).
+ * DASH_ERR_WORKSPACE: workspace_bytes < dash_attn_bwd_workspace_bytes(). */
+dash_status dash_attn_bwd(const dash_shape* shape, const void* q, const void* k, const void* v,
+                          const void* o, const void* dout, const float* lse,
+                          void* dq, void* dk, void* dv, int causal, int schedule,
+                          int deterministic, void* workspace, size_t workspace_bytes,
+                          void* stream);
+
+/* End-to-end variant with HOST buffers: q, k, v, o, dout, lse are host
+ * pointers (pinned memory recommended), dq, dk, dv host outputs.  Copies the
+ * inputs into `workspace` (device), runs dash_attn_bwd, copies the results
+ * back and synchronises `stream` before returning.  Workspace size:
+ * dash_attn_bwd_host_workspace_bytes(). */
+size_t dash_attn_bwd_host_workspace_bytes(const dash_shape* shape, int causal, int schedule,
+                                          int deterministic);
+dash_status dash_attn_bwd_host(const dash_shape* shape, const void* q, const void* k,
+                               const void* v, const void* o, const void* dout, const float* lse,
+                               void* dq, void* dk, void* dv, int causal, int schedule,
+                               int deterministic, void* workspace, size_t workspace_bytes,
+                               void* stream);
+
+/* Synchronises `stream` and reports DASH_ERR_DEADLOCK if any ticket wait in
+ * an earlier dash_attn_bwd on this workspace exceeded its spin bound (the
+ * kernel then abandons the ordered add; outputs are invalid), else DASH_OK. */
+dash_status dash_check_workspace(const dash_shape* shape, int causal, int schedule,
+                                 int deterministic, const void* workspace, void* stream);
+
+/* Host-side DAG model (§3.1-3.4): critical-path length of the
+ * deterministic backward of `n_heads` heads executed on `n_sm` SMs under
+ * `schedule`, each task a compute phase of weight c followed by a reduction
+ * phase of weight r, dQ_j reduced in the schedule's order.  Jobs are claimed
+ * head-major by the earliest-free SM, ties to the lowest SM index (AMB-7); a
+ * reduction occupies its SM (AMB-24).  n_q must equal n_kv (AMB-11).
+ * p == NULL selects {n_heads = 2, n_sm = n_kv, c = 1, r = 1}.
+ * DASH_ERR_INVALID_ARG: n_q != n_kv, n_kv < 1, c < 1 or r < 1 (positive
+ * weights: Lemma 1's premise), n_sm < 1, n_heads < 1.
+ * DASH_ERR_UNSUPPORTED: SHIFT causal with odd n_kv.
+ * DASH_ERR_DEADLOCK: the schedule cannot finish on n_sm SMs (SHIFT with
+ * fewer SMs than a head's jobs). */
+typedef struct {
+  int n_heads;
+  int n_sm;
+  int64_t c;
+  int64_t r;
+} dash_dag_params;
+
+dash_status dash_schedule_critical_path(int schedule, int n_q, int n_kv, int mask,
+                                        const dash_dag_params* p, int64_t* out_length);
+
+/* The per-head schedule table the kernels use (§8(a) row a1): for each job
+ * (in claim order) its tasks (kv tile, q tile) in visiting order and each
+ * task's rank in its dQ tile's reduction order.  Arrays must hold
+ * `capacity` tasks; *n_tasks / *n_jobs receive the counts (if capacity is
+ * too small nothing is written and DASH_ERR_WORKSPACE is returned).
+ * task_job[t] is the job index of task t; tasks of a job are contiguous. */
+dash_status dash_schedule_table(int schedule, int n_kv, int mask, int capacity,
+                                int32_t* task_job, int32_t* task_kv, int32_t* task_q,
+                                int32_t* task_rank, int32_t* n_tasks, int32_t* n_jobs);
+
+/* Number of device kernel launches one dash_attn_bwd makes (for accounting). */
+int dash_attn_bwd_launches(int causal, int schedule, int deterministic);
+
+const char* dash_status_string(dash_status s);
+const char* dash_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DASH_H_ */

@@ -1,0 +1,429 @@
+// libdash.so C ABI (include/dash.h): validation, workspace layout, TMA
+// descriptors, schedule-table cache and kernel launches.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "bwd.cuh"
+#include "dash.h"
+#include "fwd.cuh"
+#include "schedule.h"
+
+#define DASH_API extern "C" __attribute__((visibility("default")))
+
+namespace dash {
+namespace {
+
+constexpr size_t kAlign = 1024;
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+bool shape_ok(const dash_shape* s) {
+  if (!s) return false;
+  if (s->batch < 1 || s->heads < 1 || s->seqlen < 128 || s->seqlen % 128) return false;
+  if (s->head_dim != 64 && s->head_dim != 128) return false;
+  if (s->seqlen / 128 > 32767) return false;
+  return true;
+}
+bool aligned16(const void* p) { return p && (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+float eff_scale(const dash_shape* s) {
+  return s->softmax_scale > 0.f ? s->softmax_scale : 1.0f / std::sqrt(static_cast<float>(s->head_dim));
+}
+int sub_rows(int d) { return d == 128 ? BwdCfg<128>::BR : BwdCfg<64>::BR; }
+
+struct WsLayout {
+  size_t dqacc = 0, dvec = 0, tickets = 0, counters = 0, total = 0;
+  size_t dqacc_bytes = 0, n_tickets = 0;
+};
+WsLayout ws_layout(const dash_shape* s) {
+  WsLayout w;
+  const size_t BHN = static_cast<size_t>(s->batch) * s->heads * s->seqlen;
+  w.dqacc_bytes = BHN * s->head_dim * 4;
+  w.n_tickets = static_cast<size_t>(s->batch) * s->heads * (s->seqlen / sub_rows(s->head_dim));
+  size_t off = 0;
+  w.dqacc = off;
+  off = align_up(off + w.dqacc_bytes, kAlign);
+  w.dvec = off;
+  off = align_up(off + BHN * 4, kAlign);
+  w.tickets = off;
+  off = align_up(off + w.n_tickets * 4, kAlign);
+  w.counters = off;  // [0] job counter, [1] error flag
+  off = align_up(off + 64, kAlign);
+  w.total = off;
+  return w;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base,
+                 uint64_t inner, uint64_t outer, uint32_t box_inner, uint32_t box_outer) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * static_cast<uint64_t>(esize)};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int device_sms(int dev) {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  cache[dev] = n;
+  return n;
+}
+
+// Device-resident schedule tables, uploaded once per (device, key).
+struct DevTable {
+  int* job_begin = nullptr;
+  int2* tasks = nullptr;
+  int jobs = 0;
+};
+const DevTable* device_table(int dev, const ScheduleTable* t) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int>, DevTable> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_tuple(dev, t->schedule, t->n, t->mask);
+  auto it = cache.find(key);
+  if (it != cache.end()) return &it->second;
+  std::vector<int> jb(t->job_begin.begin(), t->job_begin.end());
+  std::vector<int2> tk(t->tasks.size());
+  for (size_t i = 0; i < t->tasks.size(); ++i)
+    tk[i] = make_int2(t->tasks[i].kv | (t->tasks[i].q << 16), t->tasks[i].rank);
+  DevTable d;
+  d.jobs = t->jobs;
+  void* buf = nullptr;
+  const size_t jb_bytes = align_up(jb.size() * sizeof(int), 256);
+  if (cudaMalloc(&buf, jb_bytes + tk.size() * sizeof(int2)) != cudaSuccess) return nullptr;
+  d.job_begin = static_cast<int*>(buf);
+  d.tasks = reinterpret_cast<int2*>(static_cast<char*>(buf) + jb_bytes);
+  cudaMemcpy(d.job_begin, jb.data(), jb.size() * sizeof(int), cudaMemcpyHostToDevice);
+  cudaMemcpy(d.tasks, tk.data(), tk.size() * sizeof(int2), cudaMemcpyHostToDevice);
+  cache[key] = d;
+  return &cache[key];
+}
+
+template <int D>
+dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const void* v,
+                       const void* o, const void* dout, const float* lse, void* dq, void* dk,
+                       void* dv, int causal, int schedule, int deterministic, void* workspace,
+                       cudaStream_t stream) {
+  using C = BwdCfg<D>;
+  const int n = s->seqlen / 128;
+  const ScheduleTable* tab = cached_schedule(schedule, n, causal ? kCausal : kFull);
+  if (!tab) return DASH_ERR_UNSUPPORTED;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return DASH_ERR_CUDA;
+  const int sms = device_sms(dev);
+  const int total_jobs = tab->jobs * s->batch * s->heads;
+  const int grid = total_jobs < sms ? total_jobs : sms;
+  if (schedule == kShift && tab->jobs > grid) return DASH_ERR_UNSUPPORTED;
+  const DevTable* dt = device_table(dev, tab);
+  if (!dt) return DASH_ERR_CUDA;
+
+  const WsLayout w = ws_layout(s);
+  char* ws = static_cast<char*>(workspace);
+  float* dqacc = reinterpret_cast<float*>(ws + w.dqacc);
+  float* dvec = reinterpret_cast<float*>(ws + w.dvec);
+  int* tickets = reinterpret_cast<int*>(ws + w.tickets);
+  int* counters = reinterpret_cast<int*>(ws + w.counters);
+
+  const uint64_t HD = static_cast<uint64_t>(s->heads) * D;
+  const uint64_t BN = static_cast<uint64_t>(s->batch) * s->seqlen;
+  CUtensorMap tq, tk, tv, tdo, tacc;
+  bool ok = make_map_2d(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, q, HD, BN, 64, C::BR) &&
+            make_map_2d(&tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, k, HD, BN, 64, C::BC) &&
+            make_map_2d(&tv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, v, HD, BN, 64, C::BC) &&
+            make_map_2d(&tdo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, HD, BN, 64, C::BR) &&
+            make_map_2d(&tacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dqacc, D,
+                        BN * static_cast<uint64_t>(s->heads), 32, C::BR);
+  if (!ok) return DASH_ERR_CUDA;
+
+  // K1: D, ticket / counter reset, dQacc zero-fill for the atomic variant.
+  {
+    const size_t rows = BN * s->heads;
+    const size_t threads = rows * (D / 8);
+    const int block = 256;
+    const unsigned gridp = static_cast<unsigned>((threads + block - 1) / block);
+    dash_preprocess_kernel<D><<<gridp, block, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), dvec,
+        s->batch, s->seqlen, s->heads, tickets, static_cast<int>(w.n_tickets),
+        deterministic ? nullptr : reinterpret_cast<float4*>(dqacc),
+        deterministic ? 0 : w.dqacc_bytes / 16, counters);
+  }
+  // K2: the persistent ordered-reduction backward.
+  {
+    BwdArgs a;
+    a.lse = lse;
+    a.Dvec = dvec;
+    a.dk = static_cast<__nv_bfloat16*>(dk);
+    a.dv = static_cast<__nv_bfloat16*>(dv);
+    a.tickets = tickets;
+    a.job_counter = counters;
+    a.error_flag = counters + 1;
+    a.job_begin = dt->job_begin;
+    a.tasks = dt->tasks;
+    a.B = s->batch;
+    a.N = s->seqlen;
+    a.H = s->heads;
+    a.jobs_per_head = tab->jobs;
+    a.total_jobs = total_jobs;
+    a.scale = eff_scale(s);
+    a.scale_log2 = a.scale * 1.4426950408889634f;
+    a.causal = causal ? 1 : 0;
+    a.deterministic = deterministic ? 1 : 0;
+    auto kern = dash_bwd_kernel<D>;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+      attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = C::SMEM_BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for SHIFT (AMB-12)
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tdo, tacc, a) != cudaSuccess)
+      return DASH_ERR_CUDA;
+  }
+  // K4: dQ = bf16(scale * dQacc).
+  {
+    const size_t total = BN * s->heads * (D / 8);
+    const int block = 256;
+    size_t g = (total + block - 1) / block;
+    if (g > static_cast<size_t>(sms) * 16) g = static_cast<size_t>(sms) * 16;
+    dash_dq_convert_kernel<D><<<static_cast<unsigned>(g), block, 0, stream>>>(
+        dqacc, static_cast<__nv_bfloat16*>(dq), s->batch, s->seqlen, s->heads, eff_scale(s));
+  }
+  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ERR_CUDA;
+}
+
+}  // namespace
+}  // namespace dash
+
+using namespace dash;
+
+DASH_API const char* dash_status_string(dash_status s) {
+  switch (s) {
+    case DASH_OK: return "DASH_OK";
+    case DASH_ERR_INVALID_ARG: return "DASH_ERR_INVALID_ARG";
+    case DASH_ERR_UNSUPPORTED: return "DASH_ERR_UNSUPPORTED";
+    case DASH_ERR_WORKSPACE: return "DASH_ERR_WORKSPACE";
+    case DASH_ERR_CUDA: return "DASH_ERR_CUDA";
+    case DASH_ERR_DEADLOCK: return "DASH_ERR_DEADLOCK";
+  }
+  return "DASH_ERR_UNKNOWN";
+}
+
+DASH_API const char* dash_version(void) { return "dash-b200 0.1 (sm_100a)"; }
+
+DASH_API int dash_attn_bwd_launches(int causal, int schedule, int deterministic) {
+  (void)causal;
+  (void)schedule;
+  (void)deterministic;
+  return 3;  // preprocess, main, dQ convert
+}
+
+DASH_API dash_status dash_attn_fwd(const dash_shape* s, const void* q, const void* k, const void* v,
+                                   void* o, float* lse, int causal, void* stream) {
+  if (!shape_ok(s) || !aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) ||
+      !aligned16(lse))
+    return DASH_ERR_INVALID_ARG;
+  const dim3 grid(s->seqlen / 64, s->batch * s->heads);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const float sc = eff_scale(s);
+  if (s->head_dim == 128) {
+    const size_t smem = 2 * 64 * 128 * 4;
+    cudaFuncSetAttribute(dash_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dash_fwd_kernel<128><<<grid, 256, smem, st>>>(
+        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
+        static_cast<const __nv_bfloat16*>(v), static_cast<__nv_bfloat16*>(o), lse, s->batch,
+        s->seqlen, s->heads, sc, causal ? 1 : 0);
+  } else {
+    const size_t smem = 2 * 64 * 64 * 4;
+    dash_fwd_kernel<64><<<grid, 256, smem, st>>>(
+        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
+        static_cast<const __nv_bfloat16*>(v), static_cast<__nv_bfloat16*>(o), lse, s->batch,
+        s->seqlen, s->heads, sc, causal ? 1 : 0);
+  }
+  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ERR_CUDA;
+}
+
+DASH_API size_t dash_attn_bwd_workspace_bytes(const dash_shape* s, int causal, int schedule,
+                                              int deterministic) {
+  (void)causal;
+  (void)schedule;
+  (void)deterministic;
+  if (!shape_ok(s)) return 0;
+  return ws_layout(s).total;
+}
+
+DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const void* k, const void* v,
+                                   const void* o, const void* dout, const float* lse, void* dq,
+                                   void* dk, void* dv, int causal, int schedule, int deterministic,
+                                   void* workspace, size_t workspace_bytes, void* stream) {
+  if (!shape_ok(s)) return DASH_ERR_INVALID_ARG;
+  const void* ptrs[] = {q, k, v, o, dout, lse, dq, dk, dv, workspace};
+  for (const void* p : ptrs)
+    if (!aligned16(p)) return DASH_ERR_INVALID_ARG;
+  if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_SHIFT) return DASH_ERR_INVALID_ARG;
+  if (workspace_bytes < ws_layout(s).total) return DASH_ERR_WORKSPACE;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (s->head_dim == 128)
+    return launch_bwd<128>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule, deterministic,
+                           workspace, st);
+  return launch_bwd<64>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule, deterministic,
+                        workspace, st);
+}
+
+namespace {
+struct HostWs {
+  size_t in_bytes, lse_bytes, q, k, v, o, dout, lse, dq, dk, dv, inner, total;
+};
+HostWs host_ws(const dash_shape* s) {
+  HostWs h;
+  h.in_bytes = static_cast<size_t>(s->batch) * s->seqlen * s->heads * s->head_dim * 2;
+  h.lse_bytes = static_cast<size_t>(s->batch) * s->heads * s->seqlen * 4;
+  size_t off = 0;
+  size_t* slots[] = {&h.q, &h.k, &h.v, &h.o, &h.dout, &h.dq, &h.dk, &h.dv};
+  for (size_t* sl : slots) {
+    *sl = off;
+    off = align_up(off + h.in_bytes, kAlign);
+  }
+  h.lse = off;
+  off = align_up(off + h.lse_bytes, kAlign);
+  h.inner = off;
+  h.total = off + ws_layout(s).total;
+  return h;
+}
+}  // namespace
+
+DASH_API size_t dash_attn_bwd_host_workspace_bytes(const dash_shape* s, int causal, int schedule,
+                                                   int deterministic) {
+  (void)causal;
+  (void)schedule;
+  (void)deterministic;
+  if (!shape_ok(s)) return 0;
+  return host_ws(s).total;
+}
+
+DASH_API dash_status dash_attn_bwd_host(const dash_shape* s, const void* q, const void* k,
+                                        const void* v, const void* o, const void* dout,
+                                        const float* lse, void* dq, void* dk, void* dv, int causal,
+                                        int schedule, int deterministic, void* workspace,
+                                        size_t workspace_bytes, void* stream) {
+  if (!shape_ok(s)) return DASH_ERR_INVALID_ARG;
+  const void* hptrs[] = {q, k, v, o, dout, lse, dq, dk, dv};
+  for (const void* p : hptrs)
+    if (!p) return DASH_ERR_INVALID_ARG;
+  if (!aligned16(workspace)) return DASH_ERR_INVALID_ARG;
+  const HostWs h = host_ws(s);
+  if (workspace_bytes < h.total) return DASH_ERR_WORKSPACE;
+  char* w = static_cast<char*>(workspace);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const std::pair<size_t, const void*> ins[] = {{h.q, q}, {h.k, k}, {h.v, v}, {h.o, o}, {h.dout, dout}};
+  for (auto& in : ins)
+    if (cudaMemcpyAsync(w + in.first, in.second, h.in_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return DASH_ERR_CUDA;
+  if (cudaMemcpyAsync(w + h.lse, lse, h.lse_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return DASH_ERR_CUDA;
+  dash_status r = dash_attn_bwd(s, w + h.q, w + h.k, w + h.v, w + h.o, w + h.dout,
+                                reinterpret_cast<const float*>(w + h.lse), w + h.dq, w + h.dk,
+                                w + h.dv, causal, schedule, deterministic, w + h.inner,
+                                h.total - h.inner, stream);
+  if (r != DASH_OK) return r;
+  const std::pair<void*, size_t> outs[] = {{dq, h.dq}, {dk, h.dk}, {dv, h.dv}};
+  for (auto& out : outs)
+    if (cudaMemcpyAsync(out.first, w + out.second, h.in_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      return DASH_ERR_CUDA;
+  return cudaStreamSynchronize(st) == cudaSuccess ? DASH_OK : DASH_ERR_CUDA;
+}
+
+DASH_API dash_status dash_check_workspace(const dash_shape* s, int causal, int schedule,
+                                          int deterministic, const void* workspace, void* stream) {
+  (void)causal;
+  (void)schedule;
+  (void)deterministic;
+  if (!shape_ok(s) || !workspace) return DASH_ERR_INVALID_ARG;
+  const WsLayout w = ws_layout(s);
+  int flag = 0;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int* dflag = reinterpret_cast<int*>(static_cast<char*>(const_cast<void*>(workspace)) + w.counters) + 1;
+  if (cudaMemcpyAsync(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return DASH_ERR_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return DASH_ERR_CUDA;
+  if (flag) {
+    cudaMemsetAsync(dflag, 0, sizeof(int), st);
+    cudaStreamSynchronize(st);
+    return DASH_ERR_DEADLOCK;
+  }
+  return DASH_OK;
+}
+
+DASH_API dash_status dash_schedule_critical_path(int schedule, int n_q, int n_kv, int mask,
+                                                 const dash_dag_params* p, int64_t* out_length) {
+  if (!out_length || n_q != n_kv || n_kv < 1) return DASH_ERR_INVALID_ARG;
+  if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_SHIFT) return DASH_ERR_INVALID_ARG;
+  if (mask != DASH_MASK_FULL && mask != DASH_MASK_CAUSAL) return DASH_ERR_INVALID_ARG;
+  dash_dag_params d = p ? *p : dash_dag_params{2, n_kv, 1, 1};
+  if (d.c < 1 || d.r < 1 || d.n_sm < 1 || d.n_heads < 1) return DASH_ERR_INVALID_ARG;
+  const ScheduleTable* t = cached_schedule(schedule, n_kv, mask);
+  if (!t) return DASH_ERR_UNSUPPORTED;
+  const int64_t cp = critical_path(*t, d.n_heads, d.n_sm, d.c, d.r);
+  if (cp < 0) return DASH_ERR_DEADLOCK;
+  *out_length = cp;
+  return DASH_OK;
+}
+
+DASH_API dash_status dash_schedule_table(int schedule, int n_kv, int mask, int capacity,
+                                         int32_t* task_job, int32_t* task_kv, int32_t* task_q,
+                                         int32_t* task_rank, int32_t* n_tasks, int32_t* n_jobs) {
+  if (n_kv < 1 || !n_tasks || !n_jobs) return DASH_ERR_INVALID_ARG;
+  if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_SHIFT) return DASH_ERR_INVALID_ARG;
+  if (mask != DASH_MASK_FULL && mask != DASH_MASK_CAUSAL) return DASH_ERR_INVALID_ARG;
+  const ScheduleTable* t = cached_schedule(schedule, n_kv, mask);
+  if (!t) return DASH_ERR_UNSUPPORTED;
+  *n_tasks = static_cast<int32_t>(t->tasks.size());
+  *n_jobs = t->jobs;
+  if (capacity < static_cast<int>(t->tasks.size())) return DASH_ERR_WORKSPACE;
+  if (!task_job || !task_kv || !task_q || !task_rank) return DASH_ERR_INVALID_ARG;
+  for (int j = 0; j < t->jobs; ++j)
+    for (int i = t->job_begin[j]; i < t->job_begin[j + 1]; ++i) {
+      task_job[i] = j;
+      task_kv[i] = t->tasks[i].kv;
+      task_q[i] = t->tasks[i].q;
+      task_rank[i] = t->tasks[i].rank;
+    }
+  return DASH_OK;
+}

@@ -1,0 +1,167 @@
+// Debug probes for the tcgen05 / TMA conventions the backward kernel relies
+// on (built into libdash_probe.so, used only by tests/test_gpu_probe.py).
+//
+//  * dash_probe_umma: one CTA stores A and B into SW128 tiles (K-major or
+//    MN-major, thread-written with the same swizzle formula the softmax role
+//    uses), issues one tcgen05 GEMM, reads D back from TMEM.
+//  * dash_probe_tma: TMA-loads a [rows x 64k] bf16 box with SWIZZLE_128B and
+//    dumps the raw shared-memory bytes, to pin sw128_chunk_offset().
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+#include "umma.cuh"
+
+namespace dash {
+
+template <int N, int K, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(128, 1)
+    probe_umma_kernel(const __nv_bfloat16* A, const __nv_bfloat16* Bt, float* D) {
+  constexpr int M = 128;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;                      // M*K*2 bytes
+  uint8_t* sB = smem + M * K * 2;          // N*K*2 bytes
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid / 32;
+
+  // A logical [M][K] (row-major in global).  K-major: stored [M][K];
+  // MN-major: stored [K][M].
+  for (int e = tid; e < M * K / 8; e += blockDim.x) {
+    if (!A_MN) {
+      const int r = e / (K / 8), ch = e % (K / 8);
+      const uint4 v = *reinterpret_cast<const uint4*>(A + r * K + ch * 8);
+      *reinterpret_cast<uint4*>(sA + sw128_chunk_offset(M, r, ch)) = v;
+    } else {
+      const int r = e / (M / 8), ch = e % (M / 8);  // stored row r = k index
+      __align__(16) __nv_bfloat16 tmp[8];
+      for (int t = 0; t < 8; ++t) tmp[t] = A[(ch * 8 + t) * K + r];
+      *reinterpret_cast<uint4*>(sA + sw128_chunk_offset(K, r, ch)) =
+          *reinterpret_cast<uint4*>(tmp);
+    }
+  }
+  // Bt logical [N][K] (B = Bt^T is K x N).  K-major: stored [N][K];
+  // MN-major: stored [K][N].
+  for (int e = tid; e < N * K / 8; e += blockDim.x) {
+    if (!B_MN) {
+      const int r = e / (K / 8), ch = e % (K / 8);
+      const uint4 v = *reinterpret_cast<const uint4*>(Bt + r * K + ch * 8);
+      *reinterpret_cast<uint4*>(sB + sw128_chunk_offset(N, r, ch)) = v;
+    } else {
+      const int r = e / (N / 8), ch = e % (N / 8);
+      __align__(16) __nv_bfloat16 tmp[8];
+      for (int t = 0; t < 8; ++t) tmp[t] = Bt[(ch * 8 + t) * K + r];
+      *reinterpret_cast<uint4*>(sB + sw128_chunk_offset(K, r, ch)) =
+          *reinterpret_cast<uint4*>(tmp);
+    }
+  }
+  ptx::fence_async_smem();
+  if (warp == 0) ptx::tmem_alloc<256>(&tmem_base);
+  if (tid == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbar_init();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  if (warp == 0 && ptx::elect_one()) {
+    umma_gemm<M, N, K, A_MN, B_MN>(tbase, ptx::smem_u32(sA), A_MN ? K : M, ptx::smem_u32(sB),
+                                   B_MN ? K : N, false);
+    ptx::mma_commit(&bar);
+  }
+  __syncwarp();
+  ptx::mbar_wait(&bar, 0);
+  ptx::tc_fence_after();
+  const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+  for (int c = 0; c < N; c += 32) {
+    float v[32];
+    ptx::tmem_ld32(tbase + lane_base + c, v);
+    ptx::tmem_wait_ld();
+    for (int t = 0; t < 32; ++t) D[(warp * 32 + (tid & 31)) * N + c + t] = v[t];
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) ptx::tmem_dealloc<256>(tbase);
+}
+
+__global__ void probe_tma_kernel(const __grid_constant__ CUtensorMap tmap, int rows, int cols,
+                                 uint8_t* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  const int bytes = rows * cols * 2;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ptx::mbar_arrive_expect_tx(&bar, bytes);
+    for (int b = 0; b < cols / 64; ++b)
+      ptx::tma_load_2d(smem + b * rows * 128, &tmap, &bar, b * 64, 0);
+  }
+  ptx::mbar_wait(&bar, 0);
+  for (int i = threadIdx.x; i < bytes; i += blockDim.x) out[i] = smem[i];
+}
+
+}  // namespace dash
+
+using namespace dash;
+
+extern "C" int dash_probe_umma(int n, int k, int a_mn, int b_mn, const void* A, const void* Bt,
+                               float* D) {
+  const size_t smem = 1024 + (128 * k + n * k) * 2;
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<1, 128, smem>>>(static_cast<const __nv_bfloat16*>(A),
+                           static_cast<const __nv_bfloat16*>(Bt), D);
+  };
+#define PROBE_CASE(NN, KK)                                                   \
+  if (n == NN && k == KK) {                                                  \
+    if (!a_mn && !b_mn) launch(probe_umma_kernel<NN, KK, false, false>);     \
+    if (!a_mn && b_mn) launch(probe_umma_kernel<NN, KK, false, true>);       \
+    if (a_mn && !b_mn) launch(probe_umma_kernel<NN, KK, true, false>);       \
+    if (a_mn && b_mn) launch(probe_umma_kernel<NN, KK, true, true>);         \
+  }
+  PROBE_CASE(64, 64)
+  PROBE_CASE(64, 128)
+  PROBE_CASE(128, 64)
+  PROBE_CASE(128, 128)
+#undef PROBE_CASE
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) fprintf(stderr, "dash_probe_umma: %s\n", cudaGetErrorString(e));
+  return static_cast<int>(e);
+}
+
+extern "C" int dash_probe_tma(const void* src, int rows, int cols, int ld_elems, void* out) {
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  cudaDriverEntryPointQueryResult qres;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode),
+                          cudaEnableDefault, &qres);
+  if (!encode) return -1;
+  CUtensorMap tmap;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(ld_elems), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_elems) * 2};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(src), dims,
+                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return -2;
+  const size_t smem = 1024 + rows * cols * 2;
+  cudaFuncSetAttribute(probe_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  probe_tma_kernel<<<1, 128, smem>>>(tmap, rows, cols, static_cast<uint8_t*>(out));
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return static_cast<int>(e);
+}

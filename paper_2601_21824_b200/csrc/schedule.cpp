@@ -1,0 +1,199 @@
+// Schedule tables (§8(a) row a1) and the DAG critical-path model (row a8).
+//
+// Visiting orders: NAIVE P:37/P:55/P:85-89; DESCENDING §3.3
+// P:91-103; SHIFT full §3.4 P:133 (Fig. 6); SHIFT causal = Symmetric
+// Shift §3.4 P:135-139 (Fig. 7).  Reduction ranks are closed forms
+// (DESIGN.md §Schedules): NAIVE/DESCENDING rank = i (ascending KV, AMB-6);
+// SHIFT full rank = (j - i) mod n; SHIFT causal with h = n/2:
+//   j >= h, i <  h : (j - h - i) mod h      (phase 1, cyclic rectangle)
+//   j >= h, i >= h : i                      (phase 2, right triangle)
+//   j <  h         : j - i                  (phase 2, left triangle)
+#include "schedule.h"
+
+#include <map>
+#include <mutex>
+#include <queue>
+#include <tuple>
+
+namespace dash {
+
+int ScheduleTable::max_rank_plus1(int j) const { return mask == kFull ? n : j + 1; }
+
+static int pos_mod(int a, int m) { return ((a % m) + m) % m; }
+
+bool build_schedule(int schedule, int n, int mask, ScheduleTable* out) {
+  ScheduleTable t;
+  t.n = n;
+  t.schedule = schedule;
+  t.mask = mask;
+  auto push_job = [&]() { t.job_begin.push_back(static_cast<int32_t>(t.tasks.size())); };
+  if (n < 1) return false;
+  if (schedule == kNaive || schedule == kDescending) {
+    t.jobs = n;
+    for (int i = 0; i < n; ++i) {
+      push_job();
+      const int lo = (mask == kCausal) ? i : 0;
+      for (int s = 0; s < n - lo; ++s) {
+        const int j = (schedule == kNaive) ? lo + s : n - 1 - s;
+        t.tasks.push_back({i, j, i});
+      }
+    }
+  } else if (schedule == kShift && mask == kFull) {
+    t.jobs = n;
+    for (int i = 0; i < n; ++i) {
+      push_job();
+      for (int s = 0; s < n; ++s) {
+        const int j = (i + s) % n;
+        t.tasks.push_back({i, j, pos_mod(j - i, n)});
+      }
+    }
+  } else if (schedule == kShift && mask == kCausal) {
+    if (n % 2) return false;
+    const int h = n / 2;
+    t.jobs = h;
+    for (int p = 0; p < h; ++p) {
+      push_job();
+      for (int s = 0; s <= n; ++s) {
+        int i, j;
+        if (s < h) {
+          i = p;
+          j = h + (p + s) % h;
+        } else if (s < n - p) {
+          i = p;
+          j = p + (s - h);
+        } else {
+          i = n - 1 - p;
+          j = (n - 1) - (s - (n - p));
+        }
+        int rank;
+        if (j >= h && i < h) rank = pos_mod(j - h - i, h);
+        else if (j >= h) rank = i;
+        else rank = j - i;
+        t.tasks.push_back({i, j, rank});
+      }
+    }
+  } else {
+    return false;
+  }
+  push_job();
+  *out = std::move(t);
+  return true;
+}
+
+const ScheduleTable* cached_schedule(int schedule, int n, int mask) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int>, ScheduleTable*> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_tuple(schedule, n, mask);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  auto* t = new ScheduleTable();
+  if (!build_schedule(schedule, n, mask, t)) {
+    delete t;
+    t = nullptr;
+  }
+  cache[key] = t;
+  return t;
+}
+
+// --- DAG model --------------------------------------------------------------
+// Each SM alternates compute (weight c) and reduction (weight r) phases of the
+// tasks of the job it claimed; the reduction of rank k on dQ_j of a head may
+// start only after rank k-1's reduction ended (zero-weight edge).  A
+// free SM claims the next job in head-major order; simultaneous claims go to
+// the lower SM index (AMB-7).  The makespan is the critical path.
+int64_t critical_path(const ScheduleTable& t, int m, int n_sm, int64_t c, int64_t r) {
+  const int J = t.jobs, n = t.n;
+  const int64_t total_jobs = static_cast<int64_t>(J) * m;
+  // Reduction end time of (head, j, rank); -1 = not yet started.
+  std::vector<int64_t> red_end(static_cast<size_t>(m) * n * n, -1);
+  auto slot = [&](int head, int j, int rank) {
+    return (static_cast<size_t>(head) * n + j) * n + rank;
+  };
+  struct SmState {
+    int64_t job = -1;   // global job index (head * J + local)
+    int task = 0;       // index into the job's task range
+    int64_t c_end = 0;  // compute end of the blocked task
+    bool blocked = false;
+  };
+  std::vector<SmState> sm(n_sm);
+  // blocked_on[slot] = SM waiting for that reduction to start.
+  std::vector<int> blocked_on(static_cast<size_t>(m) * n * n, -1);
+  // Event = (time, order, sm).  order: 0 compute end, 1 reduction end, 2 free.
+  using Ev = std::tuple<int64_t, int, int>;
+  std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> pq;
+  for (int s = 0; s < n_sm; ++s) pq.emplace(0, 2, s);
+  int64_t next_job = 0, makespan = 0;
+  int64_t finished_jobs = 0;
+
+  auto cur_task = [&](const SmState& st) -> const Task& {
+    return t.tasks[t.job_begin[st.job % J] + st.task];
+  };
+  // Starts the reduction of SM s's current task no earlier than `ready`;
+  // wakes the SM waiting for the next rank of the same dQ tile.
+  std::vector<std::pair<int, int64_t>> wake;  // explicit stack (sm, ready)
+  auto begin_reduction = [&](int s0, int64_t ready0) {
+    wake.emplace_back(s0, ready0);
+    while (!wake.empty()) {
+      auto [s, ready] = wake.back();
+      wake.pop_back();
+      SmState& st = sm[s];
+      const Task& tk = cur_task(st);
+      const int head = static_cast<int>(st.job / J);
+      const int64_t end = ready + r;
+      red_end[slot(head, tk.q, tk.rank)] = end;
+      st.blocked = false;
+      pq.emplace(end, 1, s);
+      const size_t nxt = slot(head, tk.q, tk.rank);
+      const int w = blocked_on[nxt];
+      if (w >= 0) {
+        blocked_on[nxt] = -1;
+        wake.emplace_back(w, std::max(sm[w].c_end, end));
+      }
+    }
+  };
+
+  while (!pq.empty()) {
+    auto [time, order, s] = pq.top();
+    pq.pop();
+    if (time > makespan) makespan = time;
+    SmState& st = sm[s];
+    if (order == 2) {
+      if (next_job >= total_jobs) {
+        st.job = -1;
+        continue;
+      }
+      st.job = next_job++;
+      st.task = 0;
+      pq.emplace(time + c, 0, s);
+    } else if (order == 0) {
+      const Task& tk = cur_task(st);
+      const int head = static_cast<int>(st.job / J);
+      if (tk.rank == 0) {
+        begin_reduction(s, time);
+      } else {
+        const int64_t pred = red_end[slot(head, tk.q, tk.rank - 1)];
+        if (pred >= 0) {
+          begin_reduction(s, std::max(time, pred));
+        } else {
+          st.blocked = true;
+          st.c_end = time;
+          blocked_on[slot(head, tk.q, tk.rank - 1)] = s;
+        }
+      }
+    } else {
+      const int ntask = t.job_begin[st.job % J + 1] - t.job_begin[st.job % J];
+      if (st.task + 1 < ntask) {
+        ++st.task;
+        pq.emplace(time + c, 0, s);
+      } else {
+        ++finished_jobs;
+        pq.emplace(time, 2, s);
+      }
+    }
+  }
+  if (finished_jobs != total_jobs) return -1;
+  return makespan;
+}
+
+}  // namespace dash

@@ -1,0 +1,210 @@
+"""Thin ctypes binding of libdash.so (include/dash.h).
+
+Argument marshalling only: every step of the attention path runs in the
+library's sm_100a kernels.  torch is used for device memory and the current
+stream.  There is no CPU fallback: if libdash.so is missing or fails to load,
+importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdash.so")
+
+NAIVE, DESCENDING, SHIFT = 0, 1, 2
+FULL, CAUSAL = 0, 1
+SCHEDULES = {"naive": NAIVE, "descending": DESCENDING, "shift": SHIFT}
+
+OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_WORKSPACE, ERR_CUDA, ERR_DEADLOCK = range(6)
+
+
+class DashError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: {status_string(status)} ({status})")
+        self.status = status
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int), ("seqlen", ctypes.c_int), ("heads", ctypes.c_int),
+                ("head_dim", ctypes.c_int), ("softmax_scale", ctypes.c_float)]
+
+
+class DagParams(ctypes.Structure):
+    _fields_ = [("n_heads", ctypes.c_int), ("n_sm", ctypes.c_int),
+                ("c", ctypes.c_int64), ("r", ctypes.c_int64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                          "(python -m paper_2601_21824_b200.build)")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i, sz, st = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t, ctypes.c_int
+    SP = ctypes.POINTER(Shape)
+    lib.dash_status_string.restype = ctypes.c_char_p
+    lib.dash_status_string.argtypes = [st]
+    lib.dash_version.restype = ctypes.c_char_p
+    lib.dash_attn_fwd.restype = st
+    lib.dash_attn_fwd.argtypes = [SP, vp, vp, vp, vp, vp, i, vp]
+    lib.dash_attn_bwd_workspace_bytes.restype = sz
+    lib.dash_attn_bwd_workspace_bytes.argtypes = [SP, i, i, i]
+    lib.dash_attn_bwd.restype = st
+    lib.dash_attn_bwd.argtypes = [SP, vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp, sz, vp]
+    lib.dash_attn_bwd_host_workspace_bytes.restype = sz
+    lib.dash_attn_bwd_host_workspace_bytes.argtypes = [SP, i, i, i]
+    lib.dash_attn_bwd_host.restype = st
+    lib.dash_attn_bwd_host.argtypes = [SP, vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp, sz, vp]
+    lib.dash_check_workspace.restype = st
+    lib.dash_check_workspace.argtypes = [SP, i, i, i, vp, vp]
+    lib.dash_schedule_critical_path.restype = st
+    lib.dash_schedule_critical_path.argtypes = [i, i, i, i, ctypes.POINTER(DagParams),
+                                                ctypes.POINTER(ctypes.c_int64)]
+    ip = ctypes.POINTER(ctypes.c_int32)
+    lib.dash_schedule_table.restype = st
+    lib.dash_schedule_table.argtypes = [i, i, i, i, ip, ip, ip, ip, ip, ip]
+    lib.dash_attn_bwd_launches.restype = i
+    lib.dash_attn_bwd_launches.argtypes = [i, i, i]
+    return lib
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def status_string(s: int) -> str:
+    return _lib.dash_status_string(int(s)).decode()
+
+
+def version() -> str:
+    return _lib.dash_version().decode()
+
+
+def _check(status: int, what: str):
+    if status != OK:
+        raise DashError(status, what)
+
+
+def _shape(q: torch.Tensor, scale):
+    B, N, H, d = q.shape
+    return Shape(B, N, H, d, float(scale) if scale else 0.0)
+
+
+def _stream(t: torch.Tensor):
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _sched(s):
+    return SCHEDULES[s] if isinstance(s, str) else int(s)
+
+
+def attn_fwd(q, k, v, causal: bool, scale=None, out=None, lse=None):
+    """dash_attn_fwd: returns (o [B,N,H,d] bf16, lse [B,H,N] fp32)."""
+    B, N, H, d = q.shape
+    o = torch.empty_like(q) if out is None else out
+    lse = torch.empty((B, H, N), device=q.device, dtype=torch.float32) if lse is None else lse
+    shp = _shape(q, scale)
+    _check(_lib.dash_attn_fwd(ctypes.byref(shp), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
+                              int(causal), _stream(q)), "dash_attn_fwd")
+    return o, lse
+
+
+def workspace_bytes(shape_bnhd, causal: bool, schedule=NAIVE, deterministic=True, scale=None) -> int:
+    B, N, H, d = shape_bnhd
+    shp = Shape(B, N, H, d, float(scale) if scale else 0.0)
+    return int(_lib.dash_attn_bwd_workspace_bytes(ctypes.byref(shp), int(causal), _sched(schedule),
+                                                  int(deterministic)))
+
+
+def alloc_workspace(shape_bnhd, causal: bool, schedule=NAIVE, deterministic=True, device="cuda"):
+    n = workspace_bytes(shape_bnhd, causal, schedule, deterministic)
+    return torch.empty(n, dtype=torch.uint8, device=device)
+
+
+def attn_bwd(q, k, v, o, dout, lse, causal: bool, schedule=NAIVE, deterministic: bool = True,
+             scale=None, workspace=None, out=None):
+    """dash_attn_bwd: returns (dq, dk, dv), bf16 [B,N,H,d]."""
+    sched = _sched(schedule)
+    if workspace is None:
+        workspace = alloc_workspace(q.shape, causal, sched, deterministic, q.device)
+    if out is None:
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    else:
+        dq, dk, dv = out
+    shp = _shape(q, scale)
+    _check(_lib.dash_attn_bwd(ctypes.byref(shp), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout),
+                              _ptr(lse), _ptr(dq), _ptr(dk), _ptr(dv), int(causal), sched,
+                              int(deterministic), _ptr(workspace), workspace.numel(), _stream(q)),
+           "dash_attn_bwd")
+    return dq, dk, dv
+
+
+def host_workspace_bytes(shape_bnhd, causal: bool, schedule=NAIVE, deterministic=True) -> int:
+    B, N, H, d = shape_bnhd
+    shp = Shape(B, N, H, d, 0.0)
+    return int(_lib.dash_attn_bwd_host_workspace_bytes(ctypes.byref(shp), int(causal),
+                                                       _sched(schedule), int(deterministic)))
+
+
+def attn_bwd_host(q, k, v, o, dout, lse, dq, dk, dv, causal: bool, schedule, deterministic,
+                  workspace, scale=None, stream=None):
+    """dash_attn_bwd_host: host (pinned) tensors in and out; synchronises."""
+    shp = _shape(q, scale)
+    s = ctypes.c_void_p(stream if stream is not None else torch.cuda.current_stream().cuda_stream)
+    _check(_lib.dash_attn_bwd_host(ctypes.byref(shp), _ptr(q), _ptr(k), _ptr(v), _ptr(o),
+                                   _ptr(dout), _ptr(lse), _ptr(dq), _ptr(dk), _ptr(dv),
+                                   int(causal), _sched(schedule), int(deterministic),
+                                   _ptr(workspace), workspace.numel(), s), "dash_attn_bwd_host")
+
+
+def check_workspace(q_shape, causal, schedule, deterministic, workspace):
+    B, N, H, d = q_shape
+    shp = Shape(B, N, H, d, 0.0)
+    return int(_lib.dash_check_workspace(ctypes.byref(shp), int(causal), _sched(schedule),
+                                         int(deterministic), _ptr(workspace),
+                                         ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+
+
+def schedule_critical_path(schedule, n_q: int, n_kv: int, mask: int, n_heads=None, n_sm=None,
+                           c: int = 1, r: int = 1) -> int:
+    """dash_schedule_critical_path (host DAG model, §3 of the paper)."""
+    out = ctypes.c_int64(0)
+    if n_heads is None and n_sm is None and c == 1 and r == 1:
+        p = None
+    else:
+        p = ctypes.byref(DagParams(2 if n_heads is None else n_heads,
+                                   n_kv if n_sm is None else n_sm, c, r))
+    _check(_lib.dash_schedule_critical_path(_sched(schedule), n_q, n_kv, mask, p,
+                                            ctypes.byref(out)), "dash_schedule_critical_path")
+    return int(out.value)
+
+
+def schedule_table(schedule, n_kv: int, mask: int):
+    """dash_schedule_table: list of jobs, each a list of (kv, q, rank)."""
+    nt, nj = ctypes.c_int32(0), ctypes.c_int32(0)
+    st = _lib.dash_schedule_table(_sched(schedule), n_kv, mask, 0, None, None, None, None,
+                                  ctypes.byref(nt), ctypes.byref(nj))
+    if st not in (OK, ERR_WORKSPACE):
+        _check(st, "dash_schedule_table")
+    n = nt.value
+    arrs = [(ctypes.c_int32 * max(n, 1))() for _ in range(4)]
+    _check(_lib.dash_schedule_table(_sched(schedule), n_kv, mask, n, *arrs, ctypes.byref(nt),
+                                    ctypes.byref(nj)), "dash_schedule_table")
+    jobs = [[] for _ in range(nj.value)]
+    for t in range(n):
+        jobs[arrs[0][t]].append((arrs[1][t], arrs[2][t], arrs[3][t]))
+    return jobs
+
+
+def bwd_launches(causal, schedule, deterministic) -> int:
+    return int(_lib.dash_attn_bwd_launches(int(causal), _sched(schedule), int(deterministic)))

@@ -1,0 +1,145 @@
+"""CPU tests of the C-ABI library: it loads, exports every declared symbol, and
+its host-side logic (schedule tables, DAG critical path, argument checks)
+matches the independent oracle bit for bit.  No GPU compute calls."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from oracle import dag_oracle as dag
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def dash():
+    from paper_2601_21824_b200 import build
+    build.build()
+    from paper_2601_21824_b200 import dash as d
+    return d
+
+
+def _declared_functions():
+    text = open(os.path.join(ROOT, "include", "dash.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(dash_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_exports_every_declared_symbol(dash):
+    names = _declared_functions()
+    assert len(names) >= 10
+    nm = subprocess.run(["nm", "-D", "--defined-only", dash.LIB_PATH], capture_output=True,
+                        text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (dash_\w+)", nm))
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    lib = ctypes.CDLL(dash.LIB_PATH)
+    for n in names:
+        getattr(lib, n)
+
+
+def test_status_strings_and_version(dash):
+    assert dash.status_string(0) == "DASH_OK"
+    assert dash.status_string(5) == "DASH_ERR_DEADLOCK"
+    assert "sm_100a" in dash.version()
+    assert dash.bwd_launches(1, dash.SHIFT, 1) >= 1
+
+
+@pytest.mark.parametrize("schedule", [dag.NAIVE, dag.DESCENDING, dag.SHIFT])
+@pytest.mark.parametrize("mask", [dag.FULL, dag.CAUSAL])
+def test_schedule_table_matches_oracle(dash, schedule, mask):
+    """The product's closed-form tables equal the oracle's definition-driven ones."""
+    for n in range(1, 70):
+        if schedule == dag.SHIFT and mask == dag.CAUSAL and n % 2:
+            with pytest.raises(dash.DashError):
+                dash.schedule_table(schedule, n, mask)
+            continue
+        jobs = dash.schedule_table(schedule, n, mask)
+        ojobs = dag.build_jobs(schedule, n, mask)
+        ranks = dag.reduction_ranks(schedule, n, mask)
+        assert len(jobs) == len(ojobs)
+        for job, ojob in zip(jobs, ojobs):
+            assert [(i, j) for i, j, _ in job] == ojob.tasks
+            assert [rk for _, _, rk in job] == [ranks[t] for t in ojob.tasks]
+
+
+def test_critical_path_matches_oracle_simulator(dash):
+    """Bit-exact int64 parity over schedule x mask x n x m x (c, r) x n_sm (T2)."""
+    checked = 0
+    for schedule in (dag.NAIVE, dag.DESCENDING, dag.SHIFT):
+        for mask in (dag.FULL, dag.CAUSAL):
+            for n in list(range(2, 17)) + [24, 32, 48, 64]:
+                if schedule == dag.SHIFT and mask == dag.CAUSAL and n % 2:
+                    continue
+                for m in (1, 2, 3, 5):
+                    for c, r in ((1, 1), (3, 1), (1, 3), (7, 4)):
+                        for n_sm in {n, max(1, n // 2 + 1), n + 3}:
+                            try:
+                                want = dag.simulate(schedule, n, mask, m, n_sm, c, r)
+                            except dag.Deadlock:
+                                with pytest.raises(dash.DashError) as e:
+                                    dash.schedule_critical_path(schedule, n, n, mask, m, n_sm, c, r)
+                                assert e.value.status == dash.ERR_DEADLOCK
+                                continue
+                            got = dash.schedule_critical_path(schedule, n, n, mask, m, n_sm, c, r)
+                            assert got == want, (schedule, mask, n, m, c, r, n_sm)
+                            checked += 1
+    assert checked > 2000
+
+
+def test_critical_path_defaults_and_errors(dash):
+    for n in (4, 16, 128):
+        assert dash.schedule_critical_path(dash.NAIVE, n, n, dash.CAUSAL) == 5 * n - 1
+        assert dash.schedule_critical_path(dash.DESCENDING, n, n, dash.CAUSAL) == 3 * n + 1
+        assert dash.schedule_critical_path(dash.SHIFT, n, n, dash.FULL) == 4 * n
+        assert dash.schedule_critical_path(dash.SHIFT, n, n, dash.CAUSAL) == 2 * n + 2
+    bad = [
+        dict(schedule=0, n_q=4, n_kv=5, mask=0),
+        dict(schedule=7, n_q=4, n_kv=4, mask=0),
+        dict(schedule=0, n_q=4, n_kv=4, mask=3),
+        dict(schedule=0, n_q=4, n_kv=4, mask=0, c=0),
+        dict(schedule=0, n_q=4, n_kv=4, mask=0, r=0),
+        dict(schedule=0, n_q=4, n_kv=4, mask=0, n_sm=0),
+    ]
+    for kw in bad:
+        with pytest.raises(dash.DashError) as e:
+            dash.schedule_critical_path(**kw)
+        assert e.value.status == dash.ERR_INVALID_ARG
+    with pytest.raises(dash.DashError) as e:
+        dash.schedule_critical_path(dash.SHIFT, 5, 5, dash.CAUSAL)
+    assert e.value.status == dash.ERR_UNSUPPORTED
+    with pytest.raises(dash.DashError) as e:
+        dash.schedule_critical_path(dash.SHIFT, 8, 8, dash.FULL, n_heads=2, n_sm=7)
+    assert e.value.status == dash.ERR_DEADLOCK
+
+
+def test_workspace_bytes_and_shape_checks(dash):
+    ws = dash.workspace_bytes((2, 1024, 16, 128), True)
+    assert ws >= 2 * 16 * 1024 * 128 * 4 + 2 * 16 * 1024 * 4
+    assert dash.workspace_bytes((2, 1000, 16, 128), True) == 0      # N % 128 != 0
+    assert dash.workspace_bytes((2, 1024, 16, 96), True) == 0       # d not in {64, 128}
+    assert dash.workspace_bytes((0, 1024, 16, 128), True) == 0
+    assert dash.host_workspace_bytes((1, 256, 1, 64), False) > dash.workspace_bytes((1, 256, 1, 64), False)
+
+
+def test_bwd_rejects_bad_arguments_without_gpu(dash):
+    """Argument validation happens before any device call."""
+    lib = dash.lib()
+    shp = dash.Shape(1, 256, 1, 64, 0.0)
+    p = ctypes.c_void_p(1 << 20)  # aligned dummy address, never dereferenced
+    nul = ctypes.c_void_p(0)
+    args = [p] * 9
+    st = lib.dash_attn_bwd(ctypes.byref(shp), nul, *args[1:], 0, 0, 1, p, 1 << 30, nul)
+    assert st == dash.ERR_INVALID_ARG
+    st = lib.dash_attn_bwd(ctypes.byref(shp), ctypes.c_void_p((1 << 20) + 4), *args[1:], 0, 0, 1, p,
+                           1 << 30, nul)
+    assert st == dash.ERR_INVALID_ARG
+    st = lib.dash_attn_bwd(ctypes.byref(shp), *args, 0, 9, 1, p, 1 << 30, nul)
+    assert st == dash.ERR_INVALID_ARG
+    st = lib.dash_attn_bwd(ctypes.byref(shp), *args, 0, 0, 1, p, 16, nul)
+    assert st == dash.ERR_WORKSPACE
+    bad = dash.Shape(1, 200, 1, 64, 0.0)
+    st = lib.dash_attn_bwd(ctypes.byref(bad), *args, 0, 0, 1, p, 1 << 30, nul)
+    assert st == dash.ERR_INVALID_ARG
