@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""Benchmark of the DASH deterministic attention backward on B200.
+
+Workload (BASELINE.json configs[1], the metric's configuration): the FA3-style
+sweep of PAPER.md §4.1 -- 16,384 total tokens, hidden 2,048, head dim
+128, seqlen 512 .. 16,384 (B = 16384 / N, H = 16), causal mask, bf16 random
+inputs.  One "step" = one dash_attn_bwd (preprocess + main + dQ convert) at
+every sweep point, with the deterministic DASH schedule SHIFT (Symmetric
+Shift for causal).  The paper preferred Descending at causal HD128 on H800
+because Symmetric Shift spilled registers and predicted that
+TMEM would remove that penalty; on B200 Symmetric Shift is measured
+faster than Descending at every causal sweep point (see the `sweep` key).
+
+value     = sweep FLOPs / device time, FLOPs by the FlashAttention convention
+            (bwd = 2.5 x fwd = 10 B H N^2 d, causal halved; DESIGN.md AMB-17).
+e2e       = the same metric through dash_attn_bwd_host with pinned host
+            buffers (H2D of q, k, v, o, dO, lse and D2H of dq, dk, dv inside
+            the timed region).
+roofline  = the main kernel's algorithmic tile FLOPs (5 GEMMs of 2*128*128*d
+            per (KV tile, Q tile) task) / its CUDA-event
+            time, against MEASURED_PEAKS.json bf16_tflops.
+sweep     = per-seqlen TFLOP/s of NAIVE / DESCENDING / SHIFT (deterministic)
+            and the atomic variant, with the gap-closure ratio (AMB-19).
+
+Multi-GPU (torchrun): weak scaling -- every rank owns H (b, h) heads of a
+G*H-head problem (sharding by heads needs no collective);
+value = all ranks' FLOPs / max-over-ranks time.
+
+--impl reference times the fp64 CPU oracle (oracle/, the correctness
+reference; there is no runnable upstream implementation) on a bounded sample
+of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEQLENS = (512, 1024, 2048, 4096, 8192, 16384)
+TOKENS, HIDDEN = 16384, 2048
+METRIC = "deterministic attn-bwd TFLOPs/s vs atomic bwd; % of B200 BF16 tensor peak"
+CPU_SAMPLE_N = 2048  # sweep point used for the oracle's bounded sample
+
+
+def fa_flops(B, N, H, d, causal):
+    f = 10.0 * B * H * N * N * d
+    return f / 2 if causal else f
+
+
+def tile_flops(B, N, H, d, causal):
+    n = N // 128
+    tasks = n * (n + 1) // 2 if causal else n * n
+    return 5 * 2.0 * 128 * 128 * d * tasks * B * H
+
+
+def shapes(head_dim, seqlens=SEQLENS):
+    return [(TOKENS // N, N, HIDDEN // head_dim, head_dim) for N in seqlens]
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append((time.time(), parts))
+
+    def mark(self, which):
+        setattr(self, which, time.time())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", float("inf"))
+        inside = [p for t, p in self.samples if t0 <= t <= t1 + 0.05]
+        window = "timed region"
+        if not inside and self.samples:  # region shorter than the sampling period
+            mid = 0.5 * (t0 + t1)
+            inside = [min(self.samples, key=lambda tp: abs(tp[0] - mid))[1]]
+            window = "nearest sample to the timed region"
+        if not inside:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        samples = inside
+        sm = [float(s[0]) for s in samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in samples for i in range(4)
+                          if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(samples), "window": window}
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    import torch
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def make_problem(B, N, H, d, causal, rank, dash, torch):
+    from paper_2601_21824_b200.inputs import attn_inputs
+    # weak scaling: rank r owns heads [r*H, (r+1)*H) of a (world*H)-head problem;
+    # drawing a per-rank seed keeps host memory per process bounded.
+    cpu = attn_inputs(B, N, H, d, seed=1000 * rank + N)
+    g = {k: v.cuda() for k, v in cpu.items()}
+    o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], causal)
+    g["o"], g["lse"] = o, lse
+    g["out"] = (torch.empty_like(g["q"]), torch.empty_like(g["k"]), torch.empty_like(g["v"]))
+    g["ws"] = dash.alloc_workspace(g["q"].shape, causal)
+    return g
+
+
+def run_bwd(dash, g, causal, schedule, det):
+    return dash.attn_bwd(g["q"], g["k"], g["v"], g["o"], g["do"], g["lse"], causal, schedule,
+                         det, workspace=g["ws"], out=g["out"])
+
+
+def time_steps(torch, fn, steps, warmup, world, before=None, after=None):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    if before:
+        before()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    if after:
+        after()
+    barrier(world)
+    return e0.elapsed_time(e1)  # ms
+
+
+def cpu_oracle_sample(head_dim, causal, heads=None):
+    """The fp64 oracle on a bounded sample: `heads` heads of the N = 2048 sweep point."""
+    import oracle
+    from paper_2601_21824_b200.inputs import attn_inputs
+    cores = len(os.sched_getaffinity(0))
+    oracle.build()
+    oracle.set_threads(cores)
+    if heads is None:
+        heads = 2 * cores
+    B, N, H, d = TOKENS // CPU_SAMPLE_N, CPU_SAMPLE_N, HIDDEN // head_dim, head_dim
+    heads = min(heads, B * H)
+    nb = max(1, heads // H)
+    nh = min(H, heads)
+    x = attn_inputs(nb, N, nh, d, seed=0)
+    f = {k: v.double().numpy() for k, v in x.items()}
+    t = time.time()
+    oracle.attn_bwd(f["q"], f["k"], f["v"], f["do"], causal)
+    dt = time.time() - t
+    fl = fa_flops(nb, N, nh, d, causal)
+    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": oracle.max_threads(),
+            "kind": "oracle", "seconds": dt,
+            "sample": f"fp64 oracle backward (C, OpenMP over heads) on {nb * nh} of the {B * H} "
+                      f"(b,h) heads of the N={N} sweep point (B={B}, H={H}, d={d}, "
+                      f"{'causal' if causal else 'full'}), FLOPs by the FA convention"}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["bf16_tflops"]), "measured burst (MEASURED_PEAKS.json bf16_tflops)"
+    return 1590.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(workload):
+    """Per-launch DRAM bytes of the main kernel from the committed ncu capture, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_main_kernel.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return j.get(workload, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def bench_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    causal = not args.full
+    cores = len(os.sched_getaffinity(0))
+    for _ in range(args.warmup):
+        cpu_oracle_sample(args.head_dim, causal, heads=cores)
+    vals, secs = [], 0.0
+    for _ in range(args.steps):
+        r = cpu_oracle_sample(args.head_dim, causal, heads=cores)
+        vals.append(r["value"])
+        secs += r["seconds"]
+    value = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * secs / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, world),
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": r["cores"], "kind": "oracle",
+                         "sample": r["sample"]},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world):
+    causal = not args.full
+    name = (f"fa3-sweep-{'causal' if causal else 'full'}-hd{args.head_dim}"
+            f"-{TOKENS}tok-hidden{HIDDEN}")
+    return {"workload": name, "seqlens": list(SEQLENS), "total_tokens": TOKENS,
+            "hidden": HIDDEN, "head_dim": args.head_dim, "mask": "causal" if causal else "full",
+            "schedule": args.schedule, "per_gpu_heads_x_batch": [list(s[::2]) for s in shapes(args.head_dim)],
+            "parallelism": f"bh-shard x{world}", "l2": "inputs > L2 (5 x 64 MiB per sweep point, 126 MB L2)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dash", choices=["dash", "reference"])
+    ap.add_argument("--head-dim", type=int, default=128)
+    ap.add_argument("--full", action="store_true", help="full mask instead of causal")
+    ap.add_argument("--schedule", default=None)
+    ap.add_argument("--no-sweep", action="store_true", help="skip the per-schedule sweep table")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--seqlens", default=None,
+                    help="comma-separated subset of the sweep (profiling only; not a bench line)")
+    args = ap.parse_args()
+    causal = not args.full
+    if args.schedule is None:
+        args.schedule = "shift"
+    if args.impl == "reference":
+        bench_reference(args)
+        return
+
+    import torch
+    world, rank, local = dist_setup(args)
+    from paper_2601_21824_b200 import dash
+    d = args.head_dim
+    seqlens = tuple(int(x) for x in args.seqlens.split(",")) if args.seqlens else SEQLENS
+    probs = [(s, make_problem(*s, causal, rank, dash, torch)) for s in shapes(d, seqlens)]
+    torch.cuda.synchronize()
+
+    def step():
+        for _, g in probs:
+            run_bwd(dash, g, causal, args.schedule, True)
+
+    flops_fa = sum(fa_flops(*s, causal) for s, _ in probs)
+    flops_tile = sum(tile_flops(*s, causal) for s, _ in probs)
+
+    # --- headline: device-timed sweep step -----------------------------------
+    prof = {}
+
+    def begin():
+        clk.mark("t0")
+        dash.profile_begin()
+
+    def end():
+        prof["ms"] = dash.profile_end()
+        clk.mark("t1")
+
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)  # let nvidia-smi start sampling before the timed region
+        ms = time_steps(torch, step, args.steps, args.warmup, world, begin, end)
+    ms_max = max_over_ranks(ms, world)
+    _, ms_main_timed, _, ncalls = prof["ms"]  # main-kernel CUDA-event time, timed calls only
+    value = world * flops_fa * args.steps / (ms_max / 1e3) / 1e12
+
+    # --- roofline of the main kernel -------------------------------------------
+    peak, peak_src = load_peaks()
+    achieved = flops_tile * args.steps / (ms_main_timed / 1e3) / 1e12
+    wl = workload_config(args, world)["workload"]
+    traffic = load_traffic(wl)
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic, "kernel": "dash_bwd_kernel",
+                "peak_source": peak_src,
+                "main_kernel_share_of_step": ms_main_timed / ms if ms > 0 else None}
+
+    # --- e2e through the host-buffer ABI call ---------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        host = []
+        for s, g in probs:
+            hb = {k: g[k].cpu().pin_memory() for k in ("q", "k", "v", "o", "do", "lse")}
+            hb["dq"], hb["dk"], hb["dv"] = (torch.empty_like(hb["q"]).pin_memory() for _ in range(3))
+            ws = torch.empty(dash.host_workspace_bytes(s, causal), dtype=torch.uint8, device="cuda")
+            host.append((s, hb, ws))
+        h2d = d2h = 0
+        for s, hb, _ in host:
+            h2d += sum(hb[k].numel() * hb[k].element_size() for k in ("q", "k", "v", "o", "do", "lse"))
+            d2h += sum(hb[k].numel() * hb[k].element_size() for k in ("dq", "dk", "dv"))
+
+        def e2e_step():
+            for s, hb, ws in host:
+                dash.attn_bwd_host(hb["q"], hb["k"], hb["v"], hb["o"], hb["do"], hb["lse"], hb["dq"],
+                                   hb["dk"], hb["dv"], causal, args.schedule, True, ws)
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier(world)
+        steps_e2e = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(steps_e2e):
+            e2e_step()
+        t1 = time.perf_counter()
+        barrier(world)
+        e2e_ms = max_over_ranks((t1 - t0) * 1e3 / steps_e2e, world)
+        e2e = {"value": world * flops_fa / (e2e_ms / 1e3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+               "steps": steps_e2e, "api": "dash_attn_bwd_host (pinned host buffers)"}
+        del host
+
+    # --- per-schedule sweep table (N = 1 only) ----------------------------------------
+    sweep = None
+    if world == 1 and not args.no_sweep:
+        sweep = []
+        for s, g in probs:
+            row = {"seqlen": s[1], "batch": s[0], "heads": s[2]}
+            f = fa_flops(*s, causal)
+            for name, sched, det in (("naive", "naive", True), ("descending", "descending", True),
+                                     ("shift", "shift", True), ("atomic", "naive", False)):
+                try:
+                    t = time_steps(torch, lambda: run_bwd(dash, g, causal, sched, det),
+                                   max(3, args.steps), 2, 1)
+                    row[name] = f * max(3, args.steps) / (t / 1e3) / 1e12
+                except dash.DashError as e:
+                    row[name] = None
+                    row[name + "_error"] = str(e)
+            best = max(v for v in (row.get("descending"), row.get("shift")) if v is not None)
+            gap = row["atomic"] - row["naive"]
+            row["best_dash"] = best
+            if abs(gap) < 0.02 * row["atomic"]:
+                row["gap_closed"] = None
+                row["pass"] = best >= 0.98 * row["naive"]
+            else:
+                row["gap_closed"] = (best - row["naive"]) / gap
+                row["pass"] = row["gap_closed"] >= 0.5
+            sweep.append(row)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_oracle_sample(d, causal)
+        cpu.pop("seconds", None)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded N(0,1) bf16 q,k,v,dO; O, L from dash_attn_fwd)",
+            "config": workload_config(args, world),
+            "frac_of_peak": value / peak,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": dash.bwd_launches(causal, args.schedule, True) * len(probs) * args.steps,
+            "clocks": clk.summary(),
+            "sweep": sweep,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -161,6 +161,31 @@ dash_status dash_schedule_table(int schedule, int n_kv, int mask, int capacity,
                                 int32_t* task_job, int32_t* task_kv, int32_t* task_q,
                                 int32_t* task_rank, int32_t* n_tasks, int32_t* n_jobs);
 
+/* Per-kernel timing of dash_attn_bwd for measurement: between
+ * dash_profile_begin() and dash_profile_end(), every dash_attn_bwd records
+ * CUDA events on its own stream around its three kernels (preprocess, main,
+ * dQ convert).  dash_profile_end synchronises those events and returns the
+ * summed milliseconds of each kernel and the number of calls profiled.
+ * Host-thread-global; not for concurrent use from several threads. */
+dash_status dash_profile_begin(void);
+dash_status dash_profile_end(double* ms_preprocess, double* ms_main, double* ms_convert,
+                             int* n_calls);
+
+/* Measurement variant of dash_attn_bwd (same arguments and results) that
+ * also records, per CTA of the main kernel and per Q sub-tile x it processes
+ * (x < trace_cap), clock64() stamps of the pipeline stages into `trace`
+ * (device memory, uint64 [grid][trace_cap][16], grid = min(jobs, SMs),
+ * zero-filled by the caller).  Slots: 0 S/dP MMAs issued, 1 P^T/dS^T seen
+ * by the MMA issuer, 2 dQ MMA issued, 3 softmax start, 4 softmax done,
+ * 5 dQ drain start, 6 dQ staged, 7 ticket acquired, 8 reduce issued,
+ * 9 ticket released.  This is the DAG model's C/R phase timeline
+ * (SURVEY.md §5 DASH_TRACE).  DASH_ERR_INVALID_ARG for a null trace. */
+dash_status dash_attn_bwd_trace(const dash_shape* shape, const void* q, const void* k,
+                                const void* v, const void* o, const void* dout, const float* lse,
+                                void* dq, void* dk, void* dv, int causal, int schedule,
+                                int deterministic, void* workspace, size_t workspace_bytes,
+                                unsigned long long* trace, int trace_cap, void* stream);
+
 /* Number of device kernel launches one dash_attn_bwd makes (for accounting). */
 int dash_attn_bwd_launches(int causal, int schedule, int deterministic);
 

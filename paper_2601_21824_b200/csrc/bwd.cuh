@@ -16,9 +16,15 @@
 //   of the fp32 partial into dQacc, release ticket = rank + 1
 //                          (Alg.1 lines 30-36)
 //
-// Warp roles (12 warps): 0 = TMA producer, 1 = MMA issuer + TMEM owner,
-// 4-7 = softmax / dS / dK-dV epilogue (TMEM lane quarter = warp % 4),
-// 8-11 = dQ drain + ordered reduction + job claiming.  Warps 2-3 idle.
+// Warp roles (16 warps, 512 threads):
+//   0      TMA producer (K/V per KV tile, Q/dO/L/D per sub-tile, NSTAGE ring)
+//   1      MMA issuer (one thread) + TMEM owner
+//   2, 3   dQ reducers: lane 0 of warp 2 handles even sub-tiles, of warp 3
+//          odd ones (acquire ticket -> TMA reduce-add -> wait -> release), so
+//          two ordered adds are in flight; warp 2 also claims jobs
+//   4-11   softmax / dS, then the dK/dV epilogue: two warpgroups, each owning
+//          half of the sub-tile's columns (TMEM lane quarter = warp % 4)
+//   12-15  dQ drain: TMEM -> registers -> SW128 fp32 staging
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -28,8 +34,8 @@
 namespace dash {
 
 struct BwdArgs {
-  const float* lse;      // [B,H,N] natural log
-  const float* Dvec;     // [B,H,N] rowsum(dO*O)
+  const float* lse2;     // [B,H,N]  -L * log2(e)  (written by the preprocess kernel)
+  const float* Dvec;     // [B,H,N]  rowsum(dO * O)
   __nv_bfloat16* dk;     // [B,N,H,d]
   __nv_bfloat16* dv;     // [B,N,H,d]
   int* tickets;          // [B*H][N/BR]
@@ -44,31 +50,49 @@ struct BwdArgs {
   float scale_log2;
   int causal;
   int deterministic;
+  unsigned long long* trace;  // optional clock64 trace [grid][trace_cap][16] (measurement only)
+  int trace_cap;
 };
+
+// Per-(CTA, sub-tile) clock64 stamps for pipeline analysis; a null trace
+// pointer makes every mark a not-taken branch.
+#define DASH_TRACE_MARK(slot, xx)                                                         \
+  do {                                                                                    \
+    if (args.trace != nullptr && static_cast<int>(xx) < args.trace_cap)                   \
+      args.trace[(static_cast<size_t>(blockIdx.x) * args.trace_cap + (xx)) * 16 + (slot)] = \
+          clock64();                                                                      \
+  } while (0)
 
 template <int D>
 struct BwdCfg {
-  static constexpr int BC = 128;                 // KV tile rows (TMEM lanes)
+  static constexpr int NTHREADS = 512;
+  static constexpr int BC = 128;                    // KV tile rows (TMEM lanes)
   static constexpr int BR = (D == 128) ? 64 : 128;  // Q sub-tile rows
-  static constexpr int NSUB = 128 / BR;          // sub-tiles per schedule Q tile
-  static constexpr int NP = (D == 128) ? 2 : 1;  // P/dS smem buffers
+  static constexpr int NSUB = 128 / BR;             // sub-tiles per schedule Q tile
+  static constexpr int NSTAGE = (D == 128) ? 3 : 2; // Q/dO/L/D ring depth
+  static constexpr int NSMX = 2;                    // softmax warpgroups (column halves)
+  static constexpr int SMX_COLS = BR / NSMX;        // columns per softmax thread
   static constexpr uint32_t KV_BYTES = BC * D * 2;
   static constexpr uint32_t Q_BYTES = BR * D * 2;
   static constexpr uint32_t P_BYTES = BC * BR * 2;
   static constexpr uint32_t DQ_BYTES = BR * D * 4;
   static constexpr uint32_t OFF_K = 0;
   static constexpr uint32_t OFF_V = OFF_K + KV_BYTES;
-  static constexpr uint32_t OFF_Q = OFF_V + KV_BYTES;         // 2 stages
-  static constexpr uint32_t OFF_DO = OFF_Q + 2 * Q_BYTES;     // 2 stages
-  static constexpr uint32_t OFF_P = OFF_DO + 2 * Q_BYTES;     // NP buffers
-  static constexpr uint32_t OFF_DS = OFF_P + NP * P_BYTES;    // NP buffers
-  static constexpr uint32_t OFF_DQ = OFF_DS + NP * P_BYTES;   // fp32 SW128 staging
-  static constexpr uint32_t OFF_L = OFF_DQ + DQ_BYTES;        // 2 x BR floats
-  static constexpr uint32_t OFF_DV = OFF_L + 2 * BR * 4;      // 2 x BR floats
-  static constexpr uint32_t OFF_BAR = OFF_DV + 2 * BR * 4;
+  static constexpr uint32_t OFF_Q = OFF_V + KV_BYTES;            // NSTAGE stages
+  static constexpr uint32_t OFF_DO = OFF_Q + NSTAGE * Q_BYTES;   // NSTAGE stages
+  static constexpr uint32_t OFF_P = OFF_DO + NSTAGE * Q_BYTES;   // P^T  bf16 SW128
+  static constexpr uint32_t OFF_DS = OFF_P + P_BYTES;            // dS^T bf16 SW128
+  static constexpr uint32_t OFF_DQ = OFF_DS + P_BYTES;           // fp32 SW128 staging buffer
+  static constexpr uint32_t OFF_L = OFF_DQ + DQ_BYTES;           // NSTAGE x BR floats
+  static constexpr uint32_t OFF_DV = OFF_L + NSTAGE * BR * 4;    // NSTAGE x BR floats
+  static constexpr uint32_t OFF_BAR = OFF_DV + NSTAGE * BR * 4;
   static constexpr int NBAR = 32;
   static constexpr uint32_t OFF_MISC = OFF_BAR + NBAR * 8;
-  static constexpr uint32_t SMEM_BYTES = OFF_MISC + 64 + 1024;  // + alignment slack
+  static constexpr uint32_t BODY_BYTES = OFF_MISC + 64;
+  // Re-alignment slack for the 1024-B swizzle atoms (as much as fits; the
+  // kernel traps if the dynamic smem base needs more than it has).
+  static constexpr uint32_t SLACK = (BODY_BYTES + 1024 <= 232448) ? 1024 : (232448 - BODY_BYTES);
+  static constexpr uint32_t SMEM_BYTES = BODY_BYTES + SLACK;
   // TMEM columns
   static constexpr uint32_t T_S = 0;
   static constexpr uint32_t T_DP = BR;
@@ -77,14 +101,24 @@ struct BwdCfg {
   static constexpr uint32_t T_DQ = 2 * BR + 2 * D;  // two buffers of 64 columns
   static_assert(T_DQ + 128 == 512, "TMEM budget");
   static_assert(SMEM_BYTES <= 232448, "smem budget");
+  static_assert(SMX_COLS % 32 == 0, "softmax column split");
 };
 
-// Barrier slots
+// Barrier slots (arrival count in parentheses)
 enum : int {
-  B_JOB0 = 0, B_JOB1 = 1, B_KV_FULL = 2, B_KV_EMPTY = 3, B_Q_FULL0 = 4, B_Q_FULL1 = 5,
-  B_Q_EMPTY0 = 6, B_Q_EMPTY1 = 7, B_S_FULL = 8, B_S_EMPTY = 9, B_P_FULL0 = 10, B_P_FULL1 = 11,
-  B_P_EMPTY0 = 12, B_P_EMPTY1 = 13, B_DQ_FULL0 = 14, B_DQ_FULL1 = 15, B_DQ_EMPTY0 = 16,
-  B_DQ_EMPTY1 = 17, B_ACC_FULL = 18, B_ACC_EMPTY = 19, B_COUNT = 20
+  B_JOB0 = 0, B_JOB1 = 1,              // job slot filled (1)
+  B_KV_FULL = 2, B_KV_EMPTY = 3,       // K/V tile loaded (tx) / consumed by MMA (commit)
+  B_S_FULL = 4, B_S_EMPTY = 5,         // S^T/dP^T in TMEM (commit) / read by softmax (256)
+  B_P_FULL = 6, B_P_EMPTY = 7,         // P^T/dS^T in smem (256) / consumed by MMA (commit)
+  B_DQ_FULL0 = 8, B_DQ_FULL1 = 9,      // dQ partial in TMEM (commit)
+  B_DQ_EMPTY0 = 10, B_DQ_EMPTY1 = 11,  // TMEM dQ buffer drained (128)
+  B_ACC_FULL = 12, B_ACC_EMPTY = 13,   // dK/dV complete (commit) / drained (256)
+  B_STG_EMPTY = 14,                    // staging read by the reduce (1)
+  B_JOB_DONE = 15,                     // both reducers released the job (2)
+  B_STG_FULL0 = 16, B_STG_FULL1 = 17,  // staging written, for reducer x & 1 (128)
+  B_Q_FULL0 = 18,                      // + stage: Q/dO/L/D loaded (tx)
+  B_Q_EMPTY0 = 24,                     // + stage: stage consumed (commit)
+  B_COUNT = 30
 };
 
 __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, int c0, int c1) {
@@ -112,16 +146,32 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// Job decode shared by every role.
+struct JobView {
+  int bh, b, h, t0, t1;
+};
+__device__ __forceinline__ JobView decode_job(const BwdArgs& a, int g) {
+  JobView j;
+  j.bh = g / a.jobs_per_head;
+  const int lj = g % a.jobs_per_head;
+  j.b = j.bh / a.H;
+  j.h = j.bh % a.H;
+  j.t0 = a.job_begin[lj];
+  j.t1 = a.job_begin[lj + 1];
+  return j;
+}
+
 template <int D>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(512, 1)
     dash_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_dqacc, const BwdArgs args) {
   using C = BwdCfg<D>;
-  constexpr int BR = C::BR, NSUB = C::NSUB, NP = C::NP;
+  constexpr int BR = C::BR, NSUB = C::NSUB, NSTAGE = C::NSTAGE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  const uint32_t pad = (1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023;
+  if (pad > C::SLACK) __trap();
+  uint8_t* smem = smem_raw + pad;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_MISC);
   int* job_slot = reinterpret_cast<int*>(smem + C::OFF_MISC + 8);  // [2]
@@ -132,12 +182,14 @@ __global__ void __launch_bounds__(384, 1)
 
   if (tid == 0) {
     for (int i = 0; i < B_COUNT; ++i) ptx::mbar_init(&bars[i], 1);
-    ptx::mbar_init(&bars[B_S_EMPTY], 128);
-    ptx::mbar_init(&bars[B_P_FULL0], 128);
-    ptx::mbar_init(&bars[B_P_FULL1], 128);
+    ptx::mbar_init(&bars[B_S_EMPTY], 128 * C::NSMX);
+    ptx::mbar_init(&bars[B_P_FULL], 128 * C::NSMX);
+    ptx::mbar_init(&bars[B_ACC_EMPTY], 128 * C::NSMX);
     ptx::mbar_init(&bars[B_DQ_EMPTY0], 128);
     ptx::mbar_init(&bars[B_DQ_EMPTY1], 128);
-    ptx::mbar_init(&bars[B_ACC_EMPTY], 128);
+    ptx::mbar_init(&bars[B_STG_FULL0], 128);
+    ptx::mbar_init(&bars[B_STG_FULL1], 128);
+    ptx::mbar_init(&bars[B_JOB_DONE], 2);
     ptx::fence_mbar_init();
     ptx::fence_async_smem();
     ptx::prefetch_tmap(&tm_q);
@@ -163,11 +215,9 @@ __global__ void __launch_bounds__(384, 1)
         const int g = job_slot[it_job & 1];
         ++it_job;
         if (g >= args.total_jobs) break;
-        const int bh = g / args.jobs_per_head, lj = g % args.jobs_per_head;
-        const int b = bh / args.H, h = bh % args.H;
-        const int t0 = args.job_begin[lj], t1 = args.job_begin[lj + 1];
+        const JobView jv = decode_job(args, g);
         int prev_kv = -1;
-        for (int t = t0; t < t1; ++t) {
+        for (int t = jv.t0; t < jv.t1; ++t) {
           const int2 tk = args.tasks[t];
           const int kv = tk.x & 0xFFFF, q = tk.x >> 16;
           if (kv != prev_kv) {
@@ -176,28 +226,29 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
             for (int blk = 0; blk < D / 64; ++blk) {
               ptx::tma_load_2d(smem + C::OFF_K + blk * C::BC * 128, &tm_k, &bars[B_KV_FULL],
-                               h * D + blk * 64, b * args.N + kv * 128);
+                               jv.h * D + blk * 64, jv.b * args.N + kv * 128);
               ptx::tma_load_2d(smem + C::OFF_V + blk * C::BC * 128, &tm_v, &bars[B_KV_FULL],
-                               h * D + blk * 64, b * args.N + kv * 128);
+                               jv.h * D + blk * 64, jv.b * args.N + kv * 128);
             }
             ++kv_cnt;
             prev_kv = kv;
           }
           for (int sub = 0; sub < NSUB; ++sub) {
-            const int stage = q_cnt & 1;
-            if (q_cnt >= 2) ptx::mbar_wait(&bars[B_Q_EMPTY0 + stage], ((q_cnt >> 1) - 1) & 1);
+            const int stage = q_cnt % NSTAGE;
+            if (q_cnt >= NSTAGE)
+              ptx::mbar_wait(&bars[B_Q_EMPTY0 + stage], ((q_cnt / NSTAGE) - 1) & 1);
             uint64_t* full = &bars[B_Q_FULL0 + stage];
             ptx::mbar_arrive_expect_tx(full, 2 * C::Q_BYTES + 2 * BR * 4);
             const int row0 = q * 128 + sub * BR;
 #pragma unroll
             for (int blk = 0; blk < D / 64; ++blk) {
               ptx::tma_load_2d(smem + C::OFF_Q + stage * C::Q_BYTES + blk * BR * 128, &tm_q, full,
-                               h * D + blk * 64, b * args.N + row0);
+                               jv.h * D + blk * 64, jv.b * args.N + row0);
               ptx::tma_load_2d(smem + C::OFF_DO + stage * C::Q_BYTES + blk * BR * 128, &tm_do,
-                               full, h * D + blk * 64, b * args.N + row0);
+                               full, jv.h * D + blk * 64, jv.b * args.N + row0);
             }
-            const size_t lo = static_cast<size_t>(bh) * args.N + row0;
-            ptx::bulk_load(sL + stage * BR, args.lse + lo, BR * 4, full);
+            const size_t lo = static_cast<size_t>(jv.bh) * args.N + row0;
+            ptx::bulk_load(sL + stage * BR, args.lse2 + lo, BR * 4, full);
             ptx::bulk_load(sDv + stage * BR, args.Dvec + lo, BR * 4, full);
             ++q_cnt;
           }
@@ -209,15 +260,15 @@ __global__ void __launch_bounds__(384, 1)
     if (lane == 0) {
       uint32_t it_job = 0, kv_cnt = 0, x = 0, acc_cnt = 0;
       const uint32_t sK = ptx::smem_u32(smem + C::OFF_K), sV = ptx::smem_u32(smem + C::OFF_V);
+      const uint32_t sP = ptx::smem_u32(smem + C::OFF_P), sdS = ptx::smem_u32(smem + C::OFF_DS);
       auto sQ = [&](uint32_t st) { return ptx::smem_u32(smem + C::OFF_Q + st * C::Q_BYTES); };
       auto sdO = [&](uint32_t st) { return ptx::smem_u32(smem + C::OFF_DO + st * C::Q_BYTES); };
-      auto sP = [&](uint32_t pb) { return ptx::smem_u32(smem + C::OFF_P + pb * C::P_BYTES); };
-      auto sdS = [&](uint32_t pb) { return ptx::smem_u32(smem + C::OFF_DS + pb * C::P_BYTES); };
       auto issue_sdp = [&](uint32_t xx) {
-        const uint32_t st = xx & 1;
-        ptx::mbar_wait(&bars[B_Q_FULL0 + st], (xx >> 1) & 1);
+        const uint32_t st = xx % NSTAGE;
+        ptx::mbar_wait(&bars[B_Q_FULL0 + st], (xx / NSTAGE) & 1);
         if (xx > 0) ptx::mbar_wait(&bars[B_S_EMPTY], (xx - 1) & 1);
         ptx::tc_fence_after();
+        DASH_TRACE_MARK(0, xx);
         umma_gemm<128, BR, D, false, false>(tbase + C::T_S, sK, 128, sQ(st), BR, false);
         umma_gemm<128, BR, D, false, false>(tbase + C::T_DP, sV, 128, sdO(st), BR, false);
         ptx::mma_commit(&bars[B_S_FULL]);
@@ -227,13 +278,12 @@ __global__ void __launch_bounds__(384, 1)
         const int g = job_slot[it_job & 1];
         ++it_job;
         if (g >= args.total_jobs) break;
-        const int lj = g % args.jobs_per_head;
-        const int t0 = args.job_begin[lj], t1 = args.job_begin[lj + 1];
-        int ts = t0;
-        while (ts < t1) {
+        const JobView jv = decode_job(args, g);
+        int ts = jv.t0;
+        while (ts < jv.t1) {
           const int kv = args.tasks[ts].x & 0xFFFF;
           int te = ts + 1;
-          while (te < t1 && (args.tasks[te].x & 0xFFFF) == kv) ++te;
+          while (te < jv.t1 && (args.tasks[te].x & 0xFFFF) == kv) ++te;
           const uint32_t nsub = static_cast<uint32_t>(te - ts) * NSUB;
           ptx::mbar_wait(&bars[B_KV_FULL], kv_cnt & 1);
           ++kv_cnt;
@@ -242,29 +292,33 @@ __global__ void __launch_bounds__(384, 1)
           issue_sdp(base);
           for (uint32_t u = 0; u < nsub; ++u) {
             const uint32_t xx = base + u;
+            // S/dP of the next sub-tile go into the tensor pipe while the
+            // softmax warps turn this one into P^T / dS^T.
             if (u + 1 < nsub) issue_sdp(xx + 1);
-            const uint32_t pb = xx % NP, st = xx & 1, db = xx & 1;
-            ptx::mbar_wait(&bars[B_P_FULL0 + pb], (xx / NP) & 1);
+            const uint32_t st = xx % NSTAGE, db = xx & 1;
+            ptx::mbar_wait(&bars[B_P_FULL], xx & 1);
+            DASH_TRACE_MARK(1, xx);
             if (u == 0 && acc_cnt > 0) ptx::mbar_wait(&bars[B_ACC_EMPTY], (acc_cnt - 1) & 1);
             ptx::tc_fence_after();
             // dV += P^T dO ; dK += dS^T Q   (Alg.1 lines 25-26)
-            umma_gemm<128, D, BR, false, true>(tbase + C::T_DV, sP(pb), 128, sdO(st), BR, u > 0);
-            umma_gemm<128, D, BR, false, true>(tbase + C::T_DK, sdS(pb), 128, sQ(st), BR, u > 0);
+            umma_gemm<128, D, BR, false, true>(tbase + C::T_DV, sP, 128, sdO(st), BR, u > 0);
+            umma_gemm<128, D, BR, false, true>(tbase + C::T_DK, sdS, 128, sQ(st), BR, u > 0);
+            ptx::mma_commit(&bars[B_Q_EMPTY0 + st]);  // Q/dO no longer needed
             if (xx >= 2) {
               ptx::mbar_wait(&bars[B_DQ_EMPTY0 + db], ((xx >> 1) - 1) & 1);
               ptx::tc_fence_after();
             }
             // dQ_local (Alg.1 line 28)
             if constexpr (D == 128) {
-              umma_gemm<128, BR, 128, true, true>(tbase + C::T_DQ + db * 64, sK, 128, sdS(pb), 128,
+              umma_gemm<128, BR, 128, true, true>(tbase + C::T_DQ + db * 64, sK, 128, sdS, 128,
                                                   false);
             } else {
-              umma_gemm<128, D, 128, true, true>(tbase + C::T_DQ + db * 64, sdS(pb), 128, sK, 128,
+              umma_gemm<128, D, 128, true, true>(tbase + C::T_DQ + db * 64, sdS, 128, sK, 128,
                                                  false);
             }
+            DASH_TRACE_MARK(2, xx);
             ptx::mma_commit(&bars[B_DQ_FULL0 + db]);
-            ptx::mma_commit(&bars[B_Q_EMPTY0 + st]);
-            ptx::mma_commit(&bars[B_P_EMPTY0 + pb]);
+            ptx::mma_commit(&bars[B_P_EMPTY]);
           }
           x = base + nsub;
           ptx::mma_commit(&bars[B_KV_EMPTY]);
@@ -274,93 +328,168 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp == 2 || warp == 3) {
+    // ======================== ordered dQ reducers ==========================
+    if (lane == 0) {
+      const uint32_t rid = static_cast<uint32_t>(warp - 2);
+      const bool det = args.deterministic != 0;
+      uint32_t it_job = 0, x = 0;
+      if (rid == 0) {
+        job_slot[0] = atomicAdd(args.job_counter, 1);
+        ptx::mbar_arrive(&bars[B_JOB0]);
+      }
+      while (true) {
+        ptx::mbar_wait(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
+        const int g = job_slot[it_job & 1];
+        if (g >= args.total_jobs) break;
+        const JobView jv = decode_job(args, g);
+        for (int t = jv.t0; t < jv.t1; ++t) {
+          const int2 tk = args.tasks[t];
+          const int q = tk.x >> 16, rank = tk.y;
+          for (int sub = 0; sub < NSUB; ++sub, ++x) {
+            if ((x & 1) != rid) continue;
+            int* ticket = args.tickets + static_cast<size_t>(jv.bh) * n_sub_tiles + q * NSUB + sub;
+            if (det) {
+              // Wait until the global order grants this block its turn (Alg.1 line 33).
+              if (ptx::ld_acquire(ticket) != rank) {
+                const long long t_start = clock64();
+                while (ptx::ld_acquire(ticket) != rank) {
+                  __nanosleep(32);
+                  if (clock64() - t_start > 8 * ptx::kWatchdogCycles ||
+                      *reinterpret_cast<volatile int*>(&ptx::g_dash_abort)) {  // ~35 s bound
+                    atomicExch(args.error_flag, 1);
+                    atomicExch(&ptx::g_dash_abort, 1);
+                    break;
+                  }
+                }
+              }
+            }
+            DASH_TRACE_MARK(7, x);
+            // one barrier per reducer: never test a parity two phases ahead
+            ptx::mbar_wait(&bars[B_STG_FULL0 + rid], (x >> 1) & 1);
+            ptx::fence_async_global();
+            // Add dQ_local to dQ (Alg.1 line 34); rank 0 stores (no zero-fill needed).
+            const int grow = jv.bh * args.N + q * 128 + sub * BR;  // row of dQacc [B*H*N, D]
+            const uint8_t* stg = smem + C::OFF_DQ;
+#pragma unroll
+            for (int blk = 0; blk < D / 32; ++blk) {
+              if (det && rank == 0) {
+                tma_store_2d(&tm_dqacc, stg + blk * BR * 128, blk * 32, grow);
+              } else {
+                tma_reduce_add_2d(&tm_dqacc, stg + blk * BR * 128, blk * 32, grow);
+              }
+            }
+            ptx::bulk_commit();
+            DASH_TRACE_MARK(8, x);
+            ptx::bulk_wait_read_all();  // staging may be overwritten from here on
+            ptx::mbar_arrive(&bars[B_STG_EMPTY]);
+            ptx::bulk_wait_all();
+            if (det) {
+              ptx::fence_async_global();
+              ptx::st_release(ticket, rank + 1);  // advance the global order (Alg.1 line 35)
+            }
+            DASH_TRACE_MARK(9, x);
+          }
+        }
+        // Both reducers have released every add of this job: only now may the
+        // CTA claim its next job (greedy claiming of AMB-7, deadlock-free).
+        ptx::mbar_arrive(&bars[B_JOB_DONE]);
+        if (rid == 0) {
+          ptx::mbar_wait(&bars[B_JOB_DONE], it_job & 1);
+          job_slot[(it_job + 1) & 1] = atomicAdd(args.job_counter, 1);
+          ptx::mbar_arrive(&bars[B_JOB0 + ((it_job + 1) & 1)]);
+        }
+        ++it_job;
+      }
+    }
+  } else if (warp >= 4 && warp < 4 + 4 * C::NSMX) {
     // ======================= softmax / dS / epilogue ======================
+    const int wg = (warp - 4) >> 2;          // column half owned by this warpgroup
     const int row = (warp & 3) * 32 + lane;  // KV row within the tile = TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    constexpr int NC = C::SMX_COLS;
+    const int c_base = wg * NC;
+    uint8_t* pP = smem + C::OFF_P;
+    uint8_t* pdS = smem + C::OFF_DS;
     uint32_t it_job = 0, x = 0, acc_cnt = 0;
     while (true) {
       ptx::mbar_wait(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
       const int g = job_slot[it_job & 1];
       ++it_job;
       if (g >= args.total_jobs) break;
-      const int bh = g / args.jobs_per_head, lj = g % args.jobs_per_head;
-      const int b = bh / args.H, h = bh % args.H;
-      const int t0 = args.job_begin[lj], t1 = args.job_begin[lj + 1];
-      for (int t = t0; t < t1; ++t) {
+      const JobView jv = decode_job(args, g);
+      for (int t = jv.t0; t < jv.t1; ++t) {
         const int2 tk = args.tasks[t];
         const int kv = tk.x & 0xFFFF, q = tk.x >> 16;
         const bool diag = args.causal && (kv == q);
         for (int sub = 0; sub < NSUB; ++sub, ++x) {
-          const uint32_t st = x & 1, pb = x % NP;
+          const uint32_t st = x % NSTAGE;
           ptx::mbar_wait(&bars[B_S_FULL], x & 1);
-          ptx::mbar_wait(&bars[B_Q_FULL0 + st], (x >> 1) & 1);
-          if (x >= NP) ptx::mbar_wait(&bars[B_P_EMPTY0 + pb], ((x / NP) - 1) & 1);
+          ptx::mbar_wait(&bars[B_Q_FULL0 + st], (x / NSTAGE) & 1);
           ptx::tc_fence_after();
-          uint8_t* pP = smem + C::OFF_P + pb * C::P_BYTES;
-          uint8_t* pdS = smem + C::OFF_DS + pb * C::P_BYTES;
+          if (row == 0 && wg == 0) DASH_TRACE_MARK(3, x);
           const float* Lrow = sL + st * BR;
           const float* Drow = sDv + st * BR;
 #pragma unroll 1
-          for (int ch = 0; ch < BR / 64; ++ch) {
-            float s[64], dp[64];
-            ptx::tmem_ld32(tbase + lane_off + C::T_S + ch * 64, *reinterpret_cast<float(*)[32]>(s));
-            ptx::tmem_ld32(tbase + lane_off + C::T_S + ch * 64 + 32,
-                           *reinterpret_cast<float(*)[32]>(s + 32));
-            ptx::tmem_ld32(tbase + lane_off + C::T_DP + ch * 64, *reinterpret_cast<float(*)[32]>(dp));
-            ptx::tmem_ld32(tbase + lane_off + C::T_DP + ch * 64 + 32,
-                           *reinterpret_cast<float(*)[32]>(dp + 32));
+          for (int ch = 0; ch < NC / 32; ++ch) {
+            const int cc0 = c_base + ch * 32;  // first Q row (column) of this chunk
+            float s[32], dp[32];
+            ptx::tmem_ld32(tbase + lane_off + C::T_S + cc0, s);
+            ptx::tmem_ld32(tbase + lane_off + C::T_DP + cc0, dp);
             ptx::tmem_wait_ld();
-            if (ch == BR / 64 - 1) {
+            if (ch == NC / 32 - 1) {
               ptx::tc_fence_before();
               ptx::mbar_arrive(&bars[B_S_EMPTY]);
             }
+            uint32_t pk[16], dk2[16];
+            const int mask_from = diag ? (row - sub * BR - cc0) : -1;  // mask cols c < mask_from
 #pragma unroll
-            for (int c8 = 0; c8 < 8; ++c8) {
-              const int col0 = ch * 64 + c8 * 8;  // Q row within the sub-tile
-              const float4 la = *reinterpret_cast<const float4*>(Lrow + col0);
-              const float4 lb = *reinterpret_cast<const float4*>(Lrow + col0 + 4);
-              const float4 da = *reinterpret_cast<const float4*>(Drow + col0);
-              const float4 db = *reinterpret_cast<const float4*>(Drow + col0 + 4);
-              const float Lv[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
-              const float Dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
-              float p[8], ds[8];
+            for (int c4 = 0; c4 < 8; ++c4) {
+              const float4 l4 = *reinterpret_cast<const float4*>(Lrow + cc0 + c4 * 4);
+              const float4 d4 = *reinterpret_cast<const float4*>(Drow + cc0 + c4 * 4);
+              const float Lv[4] = {l4.x, l4.y, l4.z, l4.w};
+              const float Dv[4] = {d4.x, d4.y, d4.z, d4.w};
+              float p[4], ds[4];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const int c = c8 * 8 + e;
-                float pv = fast_exp2(fmaf(s[c], args.scale_log2, -Lv[e] * 1.4426950408889634f));
-                if (diag && row > sub * BR + col0 + e) pv = 0.f;
+              for (int e = 0; e < 4; ++e) {
+                const int c = c4 * 4 + e;
+                float pv = fast_exp2(fmaf(s[c], args.scale_log2, Lv[e]));
+                if (c < mask_from) pv = 0.f;  // causal: key row > query row
                 p[e] = pv;
                 ds[e] = pv * (dp[c] - Dv[e]);
               }
-              uint4 pk, dk4;
-              pk.x = pack_bf16(p[0], p[1]);
-              pk.y = pack_bf16(p[2], p[3]);
-              pk.z = pack_bf16(p[4], p[5]);
-              pk.w = pack_bf16(p[6], p[7]);
-              dk4.x = pack_bf16(ds[0], ds[1]);
-              dk4.y = pack_bf16(ds[2], ds[3]);
-              dk4.z = pack_bf16(ds[4], ds[5]);
-              dk4.w = pack_bf16(ds[6], ds[7]);
-              const uint32_t off = sw128_chunk_offset(128, row, col0 >> 3);
-              *reinterpret_cast<uint4*>(pP + off) = pk;
-              *reinterpret_cast<uint4*>(pdS + off) = dk4;
+              pk[c4 * 2] = pack_bf16(p[0], p[1]);
+              pk[c4 * 2 + 1] = pack_bf16(p[2], p[3]);
+              dk2[c4 * 2] = pack_bf16(ds[0], ds[1]);
+              dk2[c4 * 2 + 1] = pack_bf16(ds[2], ds[3]);
+            }
+            // The P^T/dS^T buffer is free once the MMAs of the previous
+            // sub-tile completed; everything above overlapped with them.
+            if (ch == 0 && x > 0) ptx::mbar_wait(&bars[B_P_EMPTY], (x - 1) & 1);
+#pragma unroll
+            for (int c8 = 0; c8 < 4; ++c8) {
+              const uint32_t off = sw128_chunk_offset(128, row, (cc0 + c8 * 8) >> 3);
+              *reinterpret_cast<uint4*>(pP + off) =
+                  make_uint4(pk[c8 * 4], pk[c8 * 4 + 1], pk[c8 * 4 + 2], pk[c8 * 4 + 3]);
+              *reinterpret_cast<uint4*>(pdS + off) =
+                  make_uint4(dk2[c8 * 4], dk2[c8 * 4 + 1], dk2[c8 * 4 + 2], dk2[c8 * 4 + 3]);
             }
           }
           ptx::fence_async_smem();
-          ptx::mbar_arrive(&bars[B_P_FULL0 + pb]);
+          ptx::mbar_arrive(&bars[B_P_FULL]);
+          if (row == 0 && wg == 0) DASH_TRACE_MARK(4, x);
         }
         // End of a KV segment: dK/dV epilogue (local reduction done).
-        const bool seg_end = (t + 1 == t1) || ((args.tasks[t + 1].x & 0xFFFF) != kv);
+        const bool seg_end = (t + 1 == jv.t1) || ((args.tasks[t + 1].x & 0xFFFF) != kv);
         if (seg_end) {
           ptx::mbar_wait(&bars[B_ACC_FULL], acc_cnt & 1);
           ++acc_cnt;
           ptx::tc_fence_after();
-          const size_t grow = (static_cast<size_t>(b) * args.N + kv * 128 + row) * args.H + h;
+          const size_t grow = (static_cast<size_t>(jv.b) * args.N + kv * 128 + row) * args.H + jv.h;
           __nv_bfloat16* dvp = args.dv + grow * D;
           __nv_bfloat16* dkp = args.dk + grow * D;
 #pragma unroll 1
-          for (int c0 = 0; c0 < D; c0 += 32) {
+          for (int c0 = wg * (D / C::NSMX); c0 < (wg + 1) * (D / C::NSMX); c0 += 32) {
             float a[32], k2[32];
             ptx::tmem_ld32(tbase + lane_off + C::T_DV + c0, a);
             ptx::tmem_ld32(tbase + lane_off + C::T_DK + c0, k2);
@@ -385,100 +514,54 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     }
-  } else if (warp >= 8) {
-    // =============== dQ drain + ordered reduction + job claim ===============
+  } else {
+    // ================== dQ drain: TMEM -> fp32 SW128 staging ==================
     const int tl = (warp & 3) * 32 + lane;  // TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const bool leader = (warp == 8 && lane == 0);
-    uint8_t* stg = smem + C::OFF_DQ;
     uint32_t it_job = 0, x = 0;
-    if (leader) {
-      job_slot[0] = atomicAdd(args.job_counter, 1);
-      ptx::mbar_arrive(&bars[B_JOB0]);
-    }
     while (true) {
       ptx::mbar_wait(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
       const int g = job_slot[it_job & 1];
       ++it_job;
       if (g >= args.total_jobs) break;
-      const int bh = g / args.jobs_per_head, lj = g % args.jobs_per_head;
-      const int t0 = args.job_begin[lj], t1 = args.job_begin[lj + 1];
-      for (int t = t0; t < t1; ++t) {
-        const int2 tk = args.tasks[t];
-        const int q = tk.x >> 16, rank = tk.y;
-        for (int sub = 0; sub < NSUB; ++sub, ++x) {
-          const uint32_t db = x & 1;
-          ptx::mbar_wait(&bars[B_DQ_FULL0 + db], (x >> 1) & 1);
-          ptx::tc_fence_after();
-          float v[64];
-          ptx::tmem_ld32(tbase + lane_off + C::T_DQ + db * 64, *reinterpret_cast<float(*)[32]>(v));
-          ptx::tmem_ld32(tbase + lane_off + C::T_DQ + db * 64 + 32,
-                         *reinterpret_cast<float(*)[32]>(v + 32));
-          ptx::tmem_wait_ld();
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(&bars[B_DQ_EMPTY0 + db]);
-          // Stage the fp32 partial as SW128 boxes of 32 columns x BR rows.
-          if constexpr (D == 128) {
-            // lane tl = d index, v[c] = Q row c
-            const int blk = tl >> 5, chunk = (tl & 31) >> 2, w = tl & 3;
+      const JobView jv = decode_job(args, g);
+      const int nx = (jv.t1 - jv.t0) * NSUB;
+      for (int u = 0; u < nx; ++u, ++x) {
+        const uint32_t db = x & 1;
+        ptx::mbar_wait(&bars[B_DQ_FULL0 + db], (x >> 1) & 1);
+        ptx::tc_fence_after();
+        if (tl == 0) DASH_TRACE_MARK(5, x);
+        float v[64];
+        ptx::tmem_ld32(tbase + lane_off + C::T_DQ + db * 64, *reinterpret_cast<float(*)[32]>(v));
+        ptx::tmem_ld32(tbase + lane_off + C::T_DQ + db * 64 + 32,
+                       *reinterpret_cast<float(*)[32]>(v + 32));
+        ptx::tmem_wait_ld();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&bars[B_DQ_EMPTY0 + db]);
+        if (x >= 1) ptx::mbar_wait(&bars[B_STG_EMPTY], (x - 1) & 1);
+        uint8_t* stg = smem + C::OFF_DQ;
+        // Stage the fp32 partial as SW128 boxes of 32 columns x BR rows.
+        if constexpr (D == 128) {
+          // lane tl = d index, v[c] = Q row c
+          const int blk = tl >> 5, chunk = (tl & 31) >> 2, w = tl & 3;
 #pragma unroll
-            for (int c = 0; c < BR; ++c) {
-              const uint32_t off = blk * BR * 128 + c * 128 + ((chunk ^ (c & 7)) << 4) + w * 4;
-              *reinterpret_cast<float*>(stg + off) = v[c];
-            }
-          } else {
-            // lane tl = Q row, v[c] = d column c
-#pragma unroll
-            for (int cc = 0; cc < 16; ++cc) {
-              const int blk = cc >> 3, chunk = cc & 7;
-              const uint32_t off = blk * BR * 128 + tl * 128 + ((chunk ^ (tl & 7)) << 4);
-              *reinterpret_cast<float4*>(stg + off) =
-                  make_float4(v[cc * 4], v[cc * 4 + 1], v[cc * 4 + 2], v[cc * 4 + 3]);
-            }
+          for (int c = 0; c < BR; ++c) {
+            const uint32_t off = blk * BR * 128 + c * 128 + ((chunk ^ (c & 7)) << 4) + w * 4;
+            *reinterpret_cast<float*>(stg + off) = v[c];
           }
-          ptx::fence_async_smem();
-          ptx::bar_sync(1, 128);
-          if (leader) {
-            int* ticket = args.tickets + static_cast<size_t>(bh) * n_sub_tiles + q * NSUB + sub;
-            const int grow = bh * args.N + q * 128 + sub * BR;  // row in dQacc [B*H*N, D]
-            const bool det = args.deterministic != 0;
-            if (det) {
-              // Wait until the global order grants this block its turn (Alg.1 line 33).
-              if (ptx::ld_acquire(ticket) != rank) {
-                const uint64_t t_start = ptx::globaltimer();
-                while (ptx::ld_acquire(ticket) != rank) {
-                  __nanosleep(64);
-                  if (ptx::globaltimer() - t_start > 20000000000ull) {  // 20 s bound
-                    atomicExch(args.error_flag, 1);
-                    break;
-                  }
-                }
-              }
-              ptx::fence_async_global();
-            }
-            // Add dQ_local to dQ (Alg.1 line 34); rank 0 stores (no zero-fill needed).
+        } else {
+          // lane tl = Q row, v[c] = d column c
 #pragma unroll
-            for (int blk = 0; blk < D / 32; ++blk) {
-              if (det && rank == 0) {
-                tma_store_2d(&tm_dqacc, stg + blk * BR * 128, blk * 32, grow);
-              } else {
-                tma_reduce_add_2d(&tm_dqacc, stg + blk * BR * 128, blk * 32, grow);
-              }
-            }
-            ptx::bulk_commit();
-            ptx::bulk_wait_all();
-            if (det) {
-              ptx::fence_async_global();
-              ptx::st_release(ticket, rank + 1);  // advance the global order (Alg.1 line 35)
-            }
+          for (int cc = 0; cc < 16; ++cc) {
+            const int blk = cc >> 3, chunk = cc & 7;
+            const uint32_t off = blk * BR * 128 + tl * 128 + ((chunk ^ (tl & 7)) << 4);
+            *reinterpret_cast<float4*>(stg + off) =
+                make_float4(v[cc * 4], v[cc * 4 + 1], v[cc * 4 + 2], v[cc * 4 + 3]);
           }
-          ptx::bar_sync(2, 128);
         }
-      }
-      // All of this job's ordered adds are released: claim the next job (AMB-7).
-      if (leader) {
-        job_slot[it_job & 1] = atomicAdd(args.job_counter, 1);
-        ptx::mbar_arrive(&bars[B_JOB0 + (it_job & 1)]);
+        ptx::fence_async_smem();
+        ptx::mbar_arrive(&bars[B_STG_FULL0 + (x & 1)]);
+        if (tl == 0) DASH_TRACE_MARK(6, x);
       }
     }
   }
@@ -489,16 +572,18 @@ __global__ void __launch_bounds__(384, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tbase);
   }
+  if (tid == 0 && *reinterpret_cast<volatile int*>(&ptx::g_dash_abort)) atomicExch(args.error_flag, 2);
 }
 
-// ----------------------------------------------------------------------------
 // K1: D = rowsum(dO o O) (Alg.1 line 1; D in R^N per AMB-2), fp32 in a
-// fixed order; also resets tickets / job counter and (atomic variant only)
-// zero-fills the dQ accumulator.
+// fixed order, and lse2 = -L * log2(e) for the exp2 form of P = exp(S - L);
+// also resets tickets / job counter and (atomic variant only) zero-fills the
+// dQ accumulator.
 template <int D>
 __global__ void dash_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
                                        const __nv_bfloat16* __restrict__ dout,
-                                       float* __restrict__ Dvec, int B, int N, int H,
+                                       const float* __restrict__ lse, float* __restrict__ Dvec,
+                                       float* __restrict__ lse2, int B, int N, int H,
                                        int* __restrict__ zero_i32, int n_zero_i32,
                                        float4* __restrict__ zero_f32, size_t n_zero_f4,
                                        int* __restrict__ job_counter) {
@@ -527,11 +612,16 @@ __global__ void dash_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
       const size_t bn = row / H;
       const int n = static_cast<int>(bn % N);
       const int b = static_cast<int>(bn / N);
-      Dvec[(static_cast<size_t>(b) * H + h) * N + n] = acc;
+      const size_t i = (static_cast<size_t>(b) * H + h) * N + n;
+      Dvec[i] = acc;
+      lse2[i] = -lse[i] * 1.4426950408889634f;
     }
   }
   const size_t nthreads = static_cast<size_t>(gridDim.x) * blockDim.x;
-  if (gtid == 0) *job_counter = 0;
+  if (gtid == 0) {
+    *job_counter = 0;
+    ptx::g_dash_abort = 0;
+  }
   for (size_t i = gtid; i < static_cast<size_t>(n_zero_i32); i += nthreads) zero_i32[i] = 0;
   for (size_t i = gtid; i < n_zero_f4; i += nthreads) zero_f32[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }

@@ -39,7 +39,7 @@ float eff_scale(const dash_shape* s) {
 int sub_rows(int d) { return d == 128 ? BwdCfg<128>::BR : BwdCfg<64>::BR; }
 
 struct WsLayout {
-  size_t dqacc = 0, dvec = 0, tickets = 0, counters = 0, total = 0;
+  size_t dqacc = 0, dvec = 0, lse2 = 0, tickets = 0, counters = 0, total = 0;
   size_t dqacc_bytes = 0, n_tickets = 0;
 };
 WsLayout ws_layout(const dash_shape* s) {
@@ -51,6 +51,8 @@ WsLayout ws_layout(const dash_shape* s) {
   w.dqacc = off;
   off = align_up(off + w.dqacc_bytes, kAlign);
   w.dvec = off;
+  off = align_up(off + BHN * 4, kAlign);
+  w.lse2 = off;
   off = align_up(off + BHN * 4, kAlign);
   w.tickets = off;
   off = align_up(off + w.n_tickets * 4, kAlign);
@@ -129,6 +131,38 @@ const DevTable* device_table(int dev, const ScheduleTable* t) {
   return &cache[key];
 }
 
+// Optional in-kernel clock64 trace (dash_attn_bwd_trace), host-thread-local.
+thread_local unsigned long long* g_trace = nullptr;
+thread_local int g_trace_cap = 0;
+
+// Optional per-kernel event timing (dash_profile_begin/end).
+struct ProfState {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;  // 4 per call
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+ProfState& prof() {
+  static ProfState p;
+  return p;
+}
+void prof_mark(cudaStream_t st) {
+  ProfState& p = prof();
+  if (!p.on) return;
+  cudaEvent_t e = p.get();
+  cudaEventRecord(e, st);
+  p.ev.push_back(e);
+}
+
 template <int D>
 dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const void* v,
                        const void* o, const void* dout, const float* lse, void* dq, void* dk,
@@ -151,6 +185,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
   char* ws = static_cast<char*>(workspace);
   float* dqacc = reinterpret_cast<float*>(ws + w.dqacc);
   float* dvec = reinterpret_cast<float*>(ws + w.dvec);
+  float* lse2 = reinterpret_cast<float*>(ws + w.lse2);
   int* tickets = reinterpret_cast<int*>(ws + w.tickets);
   int* counters = reinterpret_cast<int*>(ws + w.counters);
 
@@ -165,6 +200,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
                         BN * static_cast<uint64_t>(s->heads), 32, C::BR);
   if (!ok) return DASH_ERR_CUDA;
 
+  prof_mark(stream);
   // K1: D, ticket / counter reset, dQacc zero-fill for the atomic variant.
   {
     const size_t rows = BN * s->heads;
@@ -172,15 +208,16 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     const int block = 256;
     const unsigned gridp = static_cast<unsigned>((threads + block - 1) / block);
     dash_preprocess_kernel<D><<<gridp, block, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), dvec,
-        s->batch, s->seqlen, s->heads, tickets, static_cast<int>(w.n_tickets),
+        static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse, dvec,
+        lse2, s->batch, s->seqlen, s->heads, tickets, static_cast<int>(w.n_tickets),
         deterministic ? nullptr : reinterpret_cast<float4*>(dqacc),
         deterministic ? 0 : w.dqacc_bytes / 16, counters);
   }
+  prof_mark(stream);
   // K2: the persistent ordered-reduction backward.
   {
     BwdArgs a;
-    a.lse = lse;
+    a.lse2 = lse2;
     a.Dvec = dvec;
     a.dk = static_cast<__nv_bfloat16*>(dk);
     a.dv = static_cast<__nv_bfloat16*>(dv);
@@ -198,6 +235,8 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     a.scale_log2 = a.scale * 1.4426950408889634f;
     a.causal = causal ? 1 : 0;
     a.deterministic = deterministic ? 1 : 0;
+    a.trace = g_trace;
+    a.trace_cap = g_trace_cap;
     auto kern = dash_bwd_kernel<D>;
     static bool attr_set = false;
     if (!attr_set) {
@@ -206,7 +245,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(384);
+    cfg.blockDim = dim3(C::NTHREADS);
     cfg.dynamicSmemBytes = C::SMEM_BYTES;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -217,6 +256,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     if (cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tdo, tacc, a) != cudaSuccess)
       return DASH_ERR_CUDA;
   }
+  prof_mark(stream);
   // K4: dQ = bf16(scale * dQacc).
   {
     const size_t total = BN * s->heads * (D / 8);
@@ -226,6 +266,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     dash_dq_convert_kernel<D><<<static_cast<unsigned>(g), block, 0, stream>>>(
         dqacc, static_cast<__nv_bfloat16*>(dq), s->batch, s->seqlen, s->heads, eff_scale(s));
   }
+  prof_mark(stream);
   return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ERR_CUDA;
 }
 
@@ -247,6 +288,39 @@ DASH_API const char* dash_status_string(dash_status s) {
 }
 
 DASH_API const char* dash_version(void) { return "dash-b200 0.1 (sm_100a)"; }
+
+DASH_API dash_status dash_profile_begin(void) {
+  ProfState& p = prof();
+  for (cudaEvent_t e : p.ev) p.pool.push_back(e);
+  p.ev.clear();
+  p.on = true;
+  return DASH_OK;
+}
+
+DASH_API dash_status dash_profile_end(double* ms_pre, double* ms_main, double* ms_post,
+                                      int* n_calls) {
+  ProfState& p = prof();
+  p.on = false;
+  double a = 0, b = 0, c = 0;
+  const size_t n = p.ev.size() / 4;
+  for (size_t i = 0; i < n; ++i) {
+    float t0 = 0, t1 = 0, t2 = 0;
+    if (cudaEventSynchronize(p.ev[4 * i + 3]) != cudaSuccess) return DASH_ERR_CUDA;
+    cudaEventElapsedTime(&t0, p.ev[4 * i], p.ev[4 * i + 1]);
+    cudaEventElapsedTime(&t1, p.ev[4 * i + 1], p.ev[4 * i + 2]);
+    cudaEventElapsedTime(&t2, p.ev[4 * i + 2], p.ev[4 * i + 3]);
+    a += t0;
+    b += t1;
+    c += t2;
+  }
+  for (cudaEvent_t e : p.ev) p.pool.push_back(e);
+  p.ev.clear();
+  if (ms_pre) *ms_pre = a;
+  if (ms_main) *ms_main = b;
+  if (ms_post) *ms_post = c;
+  if (n_calls) *n_calls = static_cast<int>(n);
+  return DASH_OK;
+}
 
 DASH_API int dash_attn_bwd_launches(int causal, int schedule, int deterministic) {
   (void)causal;
@@ -305,6 +379,22 @@ DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const voi
                            workspace, st);
   return launch_bwd<64>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule, deterministic,
                         workspace, st);
+}
+
+DASH_API dash_status dash_attn_bwd_trace(const dash_shape* s, const void* q, const void* k,
+                                         const void* v, const void* o, const void* dout,
+                                         const float* lse, void* dq, void* dk, void* dv, int causal,
+                                         int schedule, int deterministic, void* workspace,
+                                         size_t workspace_bytes, unsigned long long* trace,
+                                         int trace_cap, void* stream) {
+  if (!trace || trace_cap < 1) return DASH_ERR_INVALID_ARG;
+  g_trace = trace;
+  g_trace_cap = trace_cap;
+  const dash_status r = dash_attn_bwd(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule,
+                                      deterministic, workspace, workspace_bytes, stream);
+  g_trace = nullptr;
+  g_trace_cap = 0;
+  return r;
 }
 
 namespace {

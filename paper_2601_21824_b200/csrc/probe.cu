@@ -116,7 +116,7 @@ __global__ void probe_tma_kernel(const __grid_constant__ CUtensorMap tmap, int r
 
 using namespace dash;
 
-extern "C" int dash_probe_umma(int n, int k, int a_mn, int b_mn, const void* A, const void* Bt,
+extern "C" __attribute__((visibility("default"))) int dash_probe_umma(int n, int k, int a_mn, int b_mn, const void* A, const void* Bt,
                                float* D) {
   const size_t smem = 1024 + (128 * k + n * k) * 2;
   auto launch = [&](auto kern) {
@@ -142,7 +142,7 @@ extern "C" int dash_probe_umma(int n, int k, int a_mn, int b_mn, const void* A, 
   return static_cast<int>(e);
 }
 
-extern "C" int dash_probe_tma(const void* src, int rows, int cols, int ld_elems, void* out) {
+extern "C" __attribute__((visibility("default"))) int dash_probe_tma(const void* src, int rows, int cols, int ld_elems, void* out) {
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   cudaDriverEntryPointQueryResult qres;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode),

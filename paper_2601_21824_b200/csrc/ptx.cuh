@@ -3,6 +3,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cstdio>
 
 namespace dash {
 namespace ptx {
@@ -52,14 +53,29 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// Blocking wait with a watchdog: a protocol bug traps after ~10 s instead of
-// hanging the GPU (the ticket spin has its own bound, see bwd.cuh).
+// Watchdog for protocol bugs: a wait that exceeds ~4 s prints which barrier
+// it was stuck on, raises the device-wide abort flag and returns; every other
+// waiter then returns too, so the kernel ends instead of hanging the GPU.
+// (Results are invalid then; the host reports DASH_ERR_DEADLOCK.)
+__device__ int g_dash_abort;
+// clock64 (per-SM cycles, monotonic) rather than %globaltimer, which the
+// driver may re-synchronise (jump) while a kernel runs.
+constexpr long long kWatchdogCycles = 1ll << 33;  // ~4.4 s at 1.965 GHz
+__device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
+  const long long t0 = clock64();
+  while (!mbar_try_wait(bar, parity)) {
+    if (*reinterpret_cast<volatile int*>(&g_dash_abort)) return;
+    if (clock64() - t0 > kWatchdogCycles) {
+      printf("dash watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n",
+             blockIdx.x, threadIdx.x, smem_u32(bar), parity);
+      atomicExch(&g_dash_abort, 1);
+      return;
+    }
+  }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
-  const uint64_t t0 = globaltimer_ns();
-  while (!mbar_try_wait(bar, parity)) {
-    if (globaltimer_ns() - t0 > 10000000000ull) __trap();
-  }
+  mbar_wait_slow(bar, parity);
 }
 
 // ---- proxy fences -----------------------------------------------------------
@@ -101,6 +117,9 @@ __device__ __forceinline__ void bulk_reduce_add_f32(void* dst, const void* src, 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");

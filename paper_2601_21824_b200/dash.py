@@ -54,6 +54,9 @@ def _load():
     lib.dash_attn_bwd_workspace_bytes.argtypes = [SP, i, i, i]
     lib.dash_attn_bwd.restype = st
     lib.dash_attn_bwd.argtypes = [SP, vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp, sz, vp]
+    lib.dash_attn_bwd_trace.restype = st
+    lib.dash_attn_bwd_trace.argtypes = [SP, vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp, sz,
+                                        vp, i, vp]
     lib.dash_attn_bwd_host_workspace_bytes.restype = sz
     lib.dash_attn_bwd_host_workspace_bytes.argtypes = [SP, i, i, i]
     lib.dash_attn_bwd_host.restype = st
@@ -66,6 +69,11 @@ def _load():
     ip = ctypes.POINTER(ctypes.c_int32)
     lib.dash_schedule_table.restype = st
     lib.dash_schedule_table.argtypes = [i, i, i, i, ip, ip, ip, ip, ip, ip]
+    lib.dash_profile_begin.restype = st
+    lib.dash_profile_begin.argtypes = []
+    dp = ctypes.POINTER(ctypes.c_double)
+    lib.dash_profile_end.restype = st
+    lib.dash_profile_end.argtypes = [dp, dp, dp, ctypes.POINTER(ctypes.c_int)]
     lib.dash_attn_bwd_launches.restype = i
     lib.dash_attn_bwd_launches.argtypes = [i, i, i]
     return lib
@@ -149,6 +157,25 @@ def attn_bwd(q, k, v, o, dout, lse, causal: bool, schedule=NAIVE, deterministic:
     return dq, dk, dv
 
 
+def attn_bwd_trace(q, k, v, o, dout, lse, causal: bool, schedule, deterministic, trace_cap=512,
+                   scale=None, workspace=None, out=None):
+    """dash_attn_bwd_trace: returns ((dq, dk, dv), trace [grid, trace_cap, 16] int64 on device)."""
+    sched = _sched(schedule)
+    if workspace is None:
+        workspace = alloc_workspace(q.shape, causal, sched, deterministic, q.device)
+    dq, dk, dv = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)) if out is None else out
+    props = torch.cuda.get_device_properties(q.device)
+    trace = torch.zeros((props.multi_processor_count, trace_cap, 16), dtype=torch.int64,
+                        device=q.device)
+    shp = _shape(q, scale)
+    _check(_lib.dash_attn_bwd_trace(ctypes.byref(shp), _ptr(q), _ptr(k), _ptr(v), _ptr(o),
+                                    _ptr(dout), _ptr(lse), _ptr(dq), _ptr(dk), _ptr(dv),
+                                    int(causal), sched, int(deterministic), _ptr(workspace),
+                                    workspace.numel(), _ptr(trace), trace_cap, _stream(q)),
+           "dash_attn_bwd_trace")
+    return (dq, dk, dv), trace
+
+
 def host_workspace_bytes(shape_bnhd, causal: bool, schedule=NAIVE, deterministic=True) -> int:
     B, N, H, d = shape_bnhd
     shp = Shape(B, N, H, d, 0.0)
@@ -204,6 +231,18 @@ def schedule_table(schedule, n_kv: int, mask: int):
     for t in range(n):
         jobs[arrs[0][t]].append((arrs[1][t], arrs[2][t], arrs[3][t]))
     return jobs
+
+
+def profile_begin():
+    _check(_lib.dash_profile_begin(), "dash_profile_begin")
+
+
+def profile_end():
+    """Returns (ms_preprocess, ms_main, ms_convert, n_calls) summed over profiled calls."""
+    a, b, c, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+    _check(_lib.dash_profile_end(ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(n)),
+           "dash_profile_end")
+    return a.value, b.value, c.value, n.value
 
 
 def bwd_launches(causal, schedule, deterministic) -> int:
