@@ -10,7 +10,8 @@
 //   dP^T = V dO^T          (TMEM)                         tcgen05 SS
 //   P^T  = exp2(S^T*scale*log2e - L*log2e) ; dS^T = P^T o (dP^T - D)
 //                          (softmax warps: TMEM -> regs -> bf16 SW128 smem)
-//   dV  += P^T dO ;  dK += dS^T Q   (TMEM accumulators, whole job)
+//   dV  += P^T dO  (P^T from TMEM, tcgen05 TS) ;  dK += dS^T Q  (SS)
+//                          (TMEM accumulators, whole job)
 //   dQ_part = dS K  (d = 64)  or  dQ_part^T = K^T dS^T  (d = 128)   (TMEM)
 //   ordered reduction: wait ticket == rank, TMA reduce-add (rank 0: store)
 //   of the fp32 partial into dQacc, release ticket = rank + 1
@@ -52,6 +53,7 @@ struct BwdArgs {
   int deterministic;
   unsigned long long* trace;  // optional clock64 trace [grid][trace_cap][16] (measurement only)
   int trace_cap;
+  int debug;  // timing experiments only (env DASH_DEBUG): bit 0 skips the dQ reduce ops
 };
 
 // Per-(CTA, sub-tile) clock64 stamps for pipeline analysis; a null trace
@@ -75,14 +77,24 @@ struct BwdCfg {
   static constexpr uint32_t KV_BYTES = BC * D * 2;
   static constexpr uint32_t Q_BYTES = BR * D * 2;
   static constexpr uint32_t P_BYTES = BC * BR * 2;
-  static constexpr uint32_t DQ_BYTES = BR * D * 4;
+  // The fp32 dQ partial of a sub-tile is staged and reduced in units of
+  // STG_ROWS rows, each with its own ticket.  (Measured: splitting the d = 128
+  // partial into 32-row halves to afford a 4-stage Q/dO ring with one dS^T
+  // buffer was slower -- the softmax then waits on the dQ MMA.)
+  static constexpr int STG_ROWS = BR;
+  static constexpr int NUNIT = BR / STG_ROWS;  // staging units per sub-tile
+  static constexpr uint32_t DQ_BYTES = STG_ROWS * D * 4;
   static constexpr uint32_t OFF_K = 0;
   static constexpr uint32_t OFF_V = OFF_K + KV_BYTES;
   static constexpr uint32_t OFF_Q = OFF_V + KV_BYTES;            // NSTAGE stages
   static constexpr uint32_t OFF_DO = OFF_Q + NSTAGE * Q_BYTES;   // NSTAGE stages
-  static constexpr uint32_t OFF_P = OFF_DO + NSTAGE * Q_BYTES;   // P^T  bf16 SW128
-  static constexpr uint32_t OFF_DS = OFF_P + P_BYTES;            // dS^T bf16 SW128
-  static constexpr uint32_t OFF_DQ = OFF_DS + P_BYTES;           // fp32 SW128 staging buffer
+  static constexpr int NDS = 2;                                  // dS^T smem buffers
+  static constexpr int NPT = 1;                                  // P^T TMEM buffers
+  // d = 128: dS^T also lives in TMEM so dK += dS^T Q runs as a TS MMA (A from
+  // TMEM, full rate, no smem read); d = 64 has no TMEM room left for it.
+  static constexpr bool DS_IN_TMEM = (D == 128);
+  static constexpr uint32_t OFF_DS = OFF_DO + NSTAGE * Q_BYTES;  // NDS x dS^T bf16 SW128
+  static constexpr uint32_t OFF_DQ = OFF_DS + NDS * P_BYTES;     // fp32 SW128 staging buffer
   static constexpr uint32_t OFF_L = OFF_DQ + DQ_BYTES;           // NSTAGE x BR floats
   static constexpr uint32_t OFF_DV = OFF_L + NSTAGE * BR * 4;    // NSTAGE x BR floats
   static constexpr uint32_t OFF_BAR = OFF_DV + NSTAGE * BR * 4;
@@ -98,8 +110,10 @@ struct BwdCfg {
   static constexpr uint32_t T_DP = BR;
   static constexpr uint32_t T_DV = 2 * BR;
   static constexpr uint32_t T_DK = 2 * BR + D;
-  static constexpr uint32_t T_DQ = 2 * BR + 2 * D;  // two buffers of 64 columns
-  static_assert(T_DQ + 128 == 512, "TMEM budget");
+  static constexpr uint32_t T_DQ = 2 * BR + 2 * D;  // 64 columns
+  static constexpr uint32_t T_PT = T_DQ + 64;       // BR/2 columns of packed bf16 P^T
+  static constexpr uint32_t T_DST = T_PT + BR / 2;  // BR/2 columns of packed bf16 dS^T (d = 128)
+  static_assert(T_PT + NPT * BR / 2 + (DS_IN_TMEM ? BR / 2 : 0) == 512, "TMEM budget");
   static_assert(SMEM_BYTES <= 232448, "smem budget");
   static_assert(SMX_COLS % 32 == 0, "softmax column split");
 };
@@ -109,15 +123,17 @@ enum : int {
   B_JOB0 = 0, B_JOB1 = 1,              // job slot filled (1)
   B_KV_FULL = 2, B_KV_EMPTY = 3,       // K/V tile loaded (tx) / consumed by MMA (commit)
   B_S_FULL = 4, B_S_EMPTY = 5,         // S^T/dP^T in TMEM (commit) / read by softmax (256)
-  B_P_FULL = 6, B_P_EMPTY = 7,         // P^T/dS^T in smem (256) / consumed by MMA (commit)
-  B_DQ_FULL0 = 8, B_DQ_FULL1 = 9,      // dQ partial in TMEM (commit)
-  B_DQ_EMPTY0 = 10, B_DQ_EMPTY1 = 11,  // TMEM dQ buffer drained (128)
+  B_P_FULL = 6,                        // P^T (TMEM) and dS^T (smem) written (256)
+  B_DQ_FULL = 7, B_DQ_EMPTY = 8,       // dQ partial in TMEM (commit) / drained (128)
+  B_PT_EMPTY0 = 9,                     // P^T TMEM buffer consumed by dV (commit)
+  B_DST_EMPTY = 10,                    // dS^T TMEM buffer consumed by dK (commit)
+  B_DS_EMPTY0 = 22, B_DS_EMPTY1 = 23,  // dS^T smem buffer consumed by dK, dQ (commit)
   B_ACC_FULL = 12, B_ACC_EMPTY = 13,   // dK/dV complete (commit) / drained (256)
   B_STG_EMPTY = 14,                    // staging read by the reduce (1)
   B_JOB_DONE = 15,                     // both reducers released the job (2)
   B_STG_FULL0 = 16, B_STG_FULL1 = 17,  // staging written, for reducer x & 1 (128)
-  B_Q_FULL0 = 18,                      // + stage: Q/dO/L/D loaded (tx)
-  B_Q_EMPTY0 = 24,                     // + stage: stage consumed (commit)
+  B_Q_FULL0 = 18,                      // + stage (<= 4): Q/dO/L/D loaded (tx)
+  B_Q_EMPTY0 = 26,                     // + stage (<= 4): stage consumed (commit)
   B_COUNT = 30
 };
 
@@ -178,15 +194,17 @@ __global__ void __launch_bounds__(512, 1)
   float* sL = reinterpret_cast<float*>(smem + C::OFF_L);
   float* sDv = reinterpret_cast<float*>(smem + C::OFF_DV);
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
+  // Provably warp-uniform warp index (shfl broadcast): lets ptxas keep role
+  // branches and everything derived from uniform values in uniform registers.
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
 
   if (tid == 0) {
     for (int i = 0; i < B_COUNT; ++i) ptx::mbar_init(&bars[i], 1);
     ptx::mbar_init(&bars[B_S_EMPTY], 128 * C::NSMX);
     ptx::mbar_init(&bars[B_P_FULL], 128 * C::NSMX);
     ptx::mbar_init(&bars[B_ACC_EMPTY], 128 * C::NSMX);
-    ptx::mbar_init(&bars[B_DQ_EMPTY0], 128);
-    ptx::mbar_init(&bars[B_DQ_EMPTY1], 128);
+    ptx::mbar_init(&bars[B_DQ_EMPTY], 128);
     ptx::mbar_init(&bars[B_STG_FULL0], 128);
     ptx::mbar_init(&bars[B_STG_FULL1], 128);
     ptx::mbar_init(&bars[B_JOB_DONE], 2);
@@ -204,30 +222,30 @@ __global__ void __launch_bounds__(512, 1)
   ptx::tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
-  const int n_sub_tiles = (args.N / 128) * NSUB;  // tickets per head
+  const int n_units = args.N / C::STG_ROWS;  // tickets per head (one per staging unit)
 
   if (warp == 0) {
     // ============================ TMA producer ============================
-    if (lane == 0) {
+    {  // whole warp converged; elect.sync issues
       uint32_t it_job = 0, kv_cnt = 0, q_cnt = 0;
       while (true) {
-        ptx::mbar_wait(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
-        const int g = job_slot[it_job & 1];
+        ptx::mbar_wait_u(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
+        const int g = __shfl_sync(0xffffffffu, job_slot[it_job & 1], 0);
         ++it_job;
-        if (g >= args.total_jobs) break;
+        if (g >= args.total_jobs || __shfl_sync(0xffffffffu, ptx::aborted(), 0)) break;
         const JobView jv = decode_job(args, g);
         int prev_kv = -1;
         for (int t = jv.t0; t < jv.t1; ++t) {
           const int2 tk = args.tasks[t];
           const int kv = tk.x & 0xFFFF, q = tk.x >> 16;
           if (kv != prev_kv) {
-            if (kv_cnt > 0) ptx::mbar_wait(&bars[B_KV_EMPTY], (kv_cnt - 1) & 1);
-            ptx::mbar_arrive_expect_tx(&bars[B_KV_FULL], 2 * C::KV_BYTES);
+            if (kv_cnt > 0) ptx::mbar_wait_u(&bars[B_KV_EMPTY], (kv_cnt - 1) & 1);
+            ptx::mbar_arrive_expect_tx_e(&bars[B_KV_FULL], 2 * C::KV_BYTES);
 #pragma unroll
             for (int blk = 0; blk < D / 64; ++blk) {
-              ptx::tma_load_2d(smem + C::OFF_K + blk * C::BC * 128, &tm_k, &bars[B_KV_FULL],
+              ptx::tma_load_2d_e(smem + C::OFF_K + blk * C::BC * 128, &tm_k, &bars[B_KV_FULL],
                                jv.h * D + blk * 64, jv.b * args.N + kv * 128);
-              ptx::tma_load_2d(smem + C::OFF_V + blk * C::BC * 128, &tm_v, &bars[B_KV_FULL],
+              ptx::tma_load_2d_e(smem + C::OFF_V + blk * C::BC * 128, &tm_v, &bars[B_KV_FULL],
                                jv.h * D + blk * 64, jv.b * args.N + kv * 128);
             }
             ++kv_cnt;
@@ -236,20 +254,21 @@ __global__ void __launch_bounds__(512, 1)
           for (int sub = 0; sub < NSUB; ++sub) {
             const int stage = q_cnt % NSTAGE;
             if (q_cnt >= NSTAGE)
-              ptx::mbar_wait(&bars[B_Q_EMPTY0 + stage], ((q_cnt / NSTAGE) - 1) & 1);
+              ptx::mbar_wait_u(&bars[B_Q_EMPTY0 + stage], ((q_cnt / NSTAGE) - 1) & 1);
             uint64_t* full = &bars[B_Q_FULL0 + stage];
-            ptx::mbar_arrive_expect_tx(full, 2 * C::Q_BYTES + 2 * BR * 4);
+            if (lane == 0) DASH_TRACE_MARK(10, q_cnt);
+            ptx::mbar_arrive_expect_tx_e(full, 2 * C::Q_BYTES + 2 * BR * 4);
             const int row0 = q * 128 + sub * BR;
 #pragma unroll
             for (int blk = 0; blk < D / 64; ++blk) {
-              ptx::tma_load_2d(smem + C::OFF_Q + stage * C::Q_BYTES + blk * BR * 128, &tm_q, full,
+              ptx::tma_load_2d_e(smem + C::OFF_Q + stage * C::Q_BYTES + blk * BR * 128, &tm_q, full,
                                jv.h * D + blk * 64, jv.b * args.N + row0);
-              ptx::tma_load_2d(smem + C::OFF_DO + stage * C::Q_BYTES + blk * BR * 128, &tm_do,
+              ptx::tma_load_2d_e(smem + C::OFF_DO + stage * C::Q_BYTES + blk * BR * 128, &tm_do,
                                full, jv.h * D + blk * 64, jv.b * args.N + row0);
             }
             const size_t lo = static_cast<size_t>(jv.bh) * args.N + row0;
-            ptx::bulk_load(sL + stage * BR, args.lse2 + lo, BR * 4, full);
-            ptx::bulk_load(sDv + stage * BR, args.Dvec + lo, BR * 4, full);
+            ptx::bulk_load_e(sL + stage * BR, args.lse2 + lo, BR * 4, full);
+            ptx::bulk_load_e(sDv + stage * BR, args.Dvec + lo, BR * 4, full);
             ++q_cnt;
           }
         }
@@ -257,35 +276,48 @@ __global__ void __launch_bounds__(512, 1)
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ==============================
-    if (lane == 0) {
+    {  // whole warp converged; elect.sync issues (keeps descriptors uniform)
       uint32_t it_job = 0, kv_cnt = 0, x = 0, acc_cnt = 0;
-      const uint32_t sK = ptx::smem_u32(smem + C::OFF_K), sV = ptx::smem_u32(smem + C::OFF_V);
-      const uint32_t sP = ptx::smem_u32(smem + C::OFF_P), sdS = ptx::smem_u32(smem + C::OFF_DS);
-      auto sQ = [&](uint32_t st) { return ptx::smem_u32(smem + C::OFF_Q + st * C::Q_BYTES); };
-      auto sdO = [&](uint32_t st) { return ptx::smem_u32(smem + C::OFF_DO + st * C::Q_BYTES); };
+      // Base descriptors of every smem operand, built once; per-stage/buffer
+      // variants differ by a constant offset (in 16-B units) added per use.
+      const uint32_t s0 = ptx::smem_u32(smem);
+      const uint64_t dK_k = tile_desc<false>(s0 + C::OFF_K, 128);   // K as K-major A
+      const uint64_t dK_mn = tile_desc<true>(s0 + C::OFF_K, 128);   // K as MN-major A/B
+      const uint64_t dV_k = tile_desc<false>(s0 + C::OFF_V, 128);
+      const uint64_t dQ_k = tile_desc<false>(s0 + C::OFF_Q, BR);    // stage 0
+      const uint64_t dQ_mn = tile_desc<true>(s0 + C::OFF_Q, BR);
+      const uint64_t ddO_k = tile_desc<false>(s0 + C::OFF_DO, BR);
+      const uint64_t ddO_mn = tile_desc<true>(s0 + C::OFF_DO, BR);
+      const uint64_t ddS_k = tile_desc<false>(s0 + C::OFF_DS, 128);  // buffer 0
+      const uint64_t ddS_mn = tile_desc<true>(s0 + C::OFF_DS, 128);
+      constexpr uint32_t Q_STEP = C::Q_BYTES / 16, DS_STEP = C::P_BYTES / 16;
       auto issue_sdp = [&](uint32_t xx) {
         const uint32_t st = xx % NSTAGE;
-        ptx::mbar_wait(&bars[B_Q_FULL0 + st], (xx / NSTAGE) & 1);
-        if (xx > 0) ptx::mbar_wait(&bars[B_S_EMPTY], (xx - 1) & 1);
+        ptx::mbar_wait_u(&bars[B_Q_FULL0 + st], (xx / NSTAGE) & 1);
+        if (xx > 0) ptx::mbar_wait_u(&bars[B_S_EMPTY], (xx - 1) & 1);
         ptx::tc_fence_after();
-        DASH_TRACE_MARK(0, xx);
-        umma_gemm<128, BR, D, false, false>(tbase + C::T_S, sK, 128, sQ(st), BR, false);
-        umma_gemm<128, BR, D, false, false>(tbase + C::T_DP, sV, 128, sdO(st), BR, false);
-        ptx::mma_commit(&bars[B_S_FULL]);
+        if (lane == 0) DASH_TRACE_MARK(0, xx);
+        umma_gemm_d<128, BR, D, false, false, 128, BR>(tbase + C::T_S, dK_k, dQ_k + st * Q_STEP,
+                                                       false);
+        umma_gemm_d<128, BR, D, false, false, 128, BR>(tbase + C::T_DP, dV_k, ddO_k + st * Q_STEP,
+                                                       false);
+        ptx::mma_commit_e(&bars[B_S_FULL]);
       };
       while (true) {
-        ptx::mbar_wait(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
-        const int g = job_slot[it_job & 1];
+        ptx::mbar_wait_u(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
+        const int g = __shfl_sync(0xffffffffu, job_slot[it_job & 1], 0);
         ++it_job;
-        if (g >= args.total_jobs) break;
+        if (g >= args.total_jobs || __shfl_sync(0xffffffffu, ptx::aborted(), 0)) break;
         const JobView jv = decode_job(args, g);
-        int ts = jv.t0;
-        while (ts < jv.t1) {
+        const int t1 = __shfl_sync(0xffffffffu, jv.t1, 0);
+        int ts = __shfl_sync(0xffffffffu, jv.t0, 0);
+        while (ts < t1) {
           const int kv = args.tasks[ts].x & 0xFFFF;
           int te = ts + 1;
-          while (te < jv.t1 && (args.tasks[te].x & 0xFFFF) == kv) ++te;
+          while (te < t1 && (args.tasks[te].x & 0xFFFF) == kv) ++te;
+          te = __shfl_sync(0xffffffffu, te, 0);
           const uint32_t nsub = static_cast<uint32_t>(te - ts) * NSUB;
-          ptx::mbar_wait(&bars[B_KV_FULL], kv_cnt & 1);
+          ptx::mbar_wait_u(&bars[B_KV_FULL], kv_cnt & 1);
           ++kv_cnt;
           ptx::tc_fence_after();
           const uint32_t base = x;
@@ -295,34 +327,44 @@ __global__ void __launch_bounds__(512, 1)
             // S/dP of the next sub-tile go into the tensor pipe while the
             // softmax warps turn this one into P^T / dS^T.
             if (u + 1 < nsub) issue_sdp(xx + 1);
-            const uint32_t st = xx % NSTAGE, db = xx & 1;
-            ptx::mbar_wait(&bars[B_P_FULL], xx & 1);
-            DASH_TRACE_MARK(1, xx);
-            if (u == 0 && acc_cnt > 0) ptx::mbar_wait(&bars[B_ACC_EMPTY], (acc_cnt - 1) & 1);
+            const uint32_t st = xx % NSTAGE, sb = xx % C::NDS, pb = xx % C::NPT;
+            ptx::mbar_wait_u(&bars[B_P_FULL], xx & 1);
+            if (lane == 0) DASH_TRACE_MARK(1, xx);
+            if (u == 0 && acc_cnt > 0) ptx::mbar_wait_u(&bars[B_ACC_EMPTY], (acc_cnt - 1) & 1);
             ptx::tc_fence_after();
-            // dV += P^T dO ; dK += dS^T Q   (Alg.1 lines 25-26)
-            umma_gemm<128, D, BR, false, true>(tbase + C::T_DV, sP, 128, sdO(st), BR, u > 0);
-            umma_gemm<128, D, BR, false, true>(tbase + C::T_DK, sdS, 128, sQ(st), BR, u > 0);
-            ptx::mma_commit(&bars[B_Q_EMPTY0 + st]);  // Q/dO no longer needed
-            if (xx >= 2) {
-              ptx::mbar_wait(&bars[B_DQ_EMPTY0 + db], ((xx >> 1) - 1) & 1);
+            // dV += P^T dO  (A = P^T straight from TMEM)   (Alg.1 line 25)
+            umma_gemm_ts_d<D, BR, true, BR>(tbase + C::T_DV, tbase + C::T_PT + pb * (BR / 2),
+                                            ddO_mn + st * Q_STEP, u > 0);
+            ptx::mma_commit_e(&bars[B_PT_EMPTY0 + pb]);
+            // dK += dS^T Q   (Alg.1 line 26)
+            if constexpr (C::DS_IN_TMEM) {
+              umma_gemm_ts_d<D, BR, true, BR>(tbase + C::T_DK, tbase + C::T_DST, dQ_mn + st * Q_STEP,
+                                              u > 0);
+              ptx::mma_commit_e(&bars[B_DST_EMPTY]);
+            } else {
+              umma_gemm_d<128, D, BR, false, true, 128, BR>(tbase + C::T_DK, ddS_k + sb * DS_STEP,
+                                                            dQ_mn + st * Q_STEP, u > 0);
+            }
+            ptx::mma_commit_e(&bars[B_Q_EMPTY0 + st]);  // Q/dO no longer needed
+            if (xx >= 1) {
+              ptx::mbar_wait_u(&bars[B_DQ_EMPTY], (xx - 1) & 1);
               ptx::tc_fence_after();
             }
             // dQ_local (Alg.1 line 28)
             if constexpr (D == 128) {
-              umma_gemm<128, BR, 128, true, true>(tbase + C::T_DQ + db * 64, sK, 128, sdS, 128,
-                                                  false);
+              umma_gemm_d<128, BR, 128, true, true, 128, 128>(tbase + C::T_DQ, dK_mn,
+                                                              ddS_mn + sb * DS_STEP, false);
             } else {
-              umma_gemm<128, D, 128, true, true>(tbase + C::T_DQ + db * 64, sdS, 128, sK, 128,
-                                                 false);
+              umma_gemm_d<128, D, 128, true, true, 128, 128>(tbase + C::T_DQ, ddS_mn + sb * DS_STEP,
+                                                             dK_mn, false);
             }
-            DASH_TRACE_MARK(2, xx);
-            ptx::mma_commit(&bars[B_DQ_FULL0 + db]);
-            ptx::mma_commit(&bars[B_P_EMPTY]);
+            if (lane == 0) DASH_TRACE_MARK(2, xx);
+            ptx::mma_commit_e(&bars[B_DQ_FULL]);
+            ptx::mma_commit_e(&bars[B_DS_EMPTY0 + sb]);
           }
           x = base + nsub;
-          ptx::mma_commit(&bars[B_KV_EMPTY]);
-          ptx::mma_commit(&bars[B_ACC_FULL]);
+          ptx::mma_commit_e(&bars[B_KV_EMPTY]);
+          ptx::mma_commit_e(&bars[B_ACC_FULL]);
           ++acc_cnt;
           ts = te;
         }
@@ -330,11 +372,11 @@ __global__ void __launch_bounds__(512, 1)
     }
   } else if (warp == 2 || warp == 3) {
     // ======================== ordered dQ reducers ==========================
-    if (lane == 0) {
+    {  // whole warp converged; one elected lane owns the bulk groups
       const uint32_t rid = static_cast<uint32_t>(warp - 2);
       const bool det = args.deterministic != 0;
       uint32_t it_job = 0, x = 0;
-      if (rid == 0) {
+      if (rid == 0 && lane == 0) {
         job_slot[0] = atomicAdd(args.job_counter, 1);
         ptx::mbar_arrive(&bars[B_JOB0]);
       }
@@ -346,9 +388,11 @@ __global__ void __launch_bounds__(512, 1)
         for (int t = jv.t0; t < jv.t1; ++t) {
           const int2 tk = args.tasks[t];
           const int q = tk.x >> 16, rank = tk.y;
-          for (int sub = 0; sub < NSUB; ++sub, ++x) {
+          for (int sub = 0; sub < NSUB; ++sub) {
+           for (int h = 0; h < C::NUNIT; ++h, ++x) {  // x counts staging units here
             if ((x & 1) != rid) continue;
-            int* ticket = args.tickets + static_cast<size_t>(jv.bh) * n_sub_tiles + q * NSUB + sub;
+            const int urow = q * 128 + sub * BR + h * C::STG_ROWS;  // first Q row of the unit
+            int* ticket = args.tickets + static_cast<size_t>(jv.bh) * n_units + urow / C::STG_ROWS;
             if (det) {
               // Wait until the global order grants this block its turn (Alg.1 line 33).
               if (ptx::ld_acquire(ticket) != rank) {
@@ -357,48 +401,61 @@ __global__ void __launch_bounds__(512, 1)
                   __nanosleep(32);
                   if (clock64() - t_start > 8 * ptx::kWatchdogCycles ||
                       *reinterpret_cast<volatile int*>(&ptx::g_dash_abort)) {  // ~35 s bound
-                    atomicExch(args.error_flag, 1);
-                    atomicExch(&ptx::g_dash_abort, 1);
+                    if (lane == 0) {
+                      atomicExch(args.error_flag, 1);
+                      atomicExch(&ptx::g_dash_abort, 1);
+                    }
                     break;
                   }
                 }
               }
             }
-            DASH_TRACE_MARK(7, x);
+            // Order the ticket acquire (generic proxy) before the reduce (async
+            // proxy); done while the partial is still being staged.
+            if (det) ptx::fence_async_global();
+            if (lane == 0 && h == 0) DASH_TRACE_MARK(7, x / C::NUNIT);
             // one barrier per reducer: never test a parity two phases ahead
             ptx::mbar_wait(&bars[B_STG_FULL0 + rid], (x >> 1) & 1);
-            ptx::fence_async_global();
+            __syncwarp();
             // Add dQ_local to dQ (Alg.1 line 34); rank 0 stores (no zero-fill needed).
-            const int grow = jv.bh * args.N + q * 128 + sub * BR;  // row of dQacc [B*H*N, D]
+            const int grow = jv.bh * args.N + urow;  // row of dQacc [B*H*N, D]
             const uint8_t* stg = smem + C::OFF_DQ;
+            if (lane == 0) {
 #pragma unroll
-            for (int blk = 0; blk < D / 32; ++blk) {
-              if (det && rank == 0) {
-                tma_store_2d(&tm_dqacc, stg + blk * BR * 128, blk * 32, grow);
-              } else {
-                tma_reduce_add_2d(&tm_dqacc, stg + blk * BR * 128, blk * 32, grow);
+              for (int blk = 0; blk < D / 32; ++blk) {
+                if (args.debug & 1) break;  // timing experiment: no reduce traffic
+                if (det && rank == 0) {
+                  tma_store_2d(&tm_dqacc, stg + blk * C::STG_ROWS * 128, blk * 32, grow);
+                } else {
+                  tma_reduce_add_2d(&tm_dqacc, stg + blk * C::STG_ROWS * 128, blk * 32, grow);
+                }
               }
+              ptx::bulk_commit();
+              if (h == 0) DASH_TRACE_MARK(8, x / C::NUNIT);
+              ptx::bulk_wait_read_all();  // staging may be overwritten from here on
+              ptx::mbar_arrive(&bars[B_STG_EMPTY]);
+              ptx::bulk_wait_all();
+              if (det) {
+                ptx::fence_async_global();
+                ptx::st_release(ticket, rank + 1);  // advance the global order (Alg.1 line 35)
+              }
+              if (h == C::NUNIT - 1) DASH_TRACE_MARK(9, x / C::NUNIT);
             }
-            ptx::bulk_commit();
-            DASH_TRACE_MARK(8, x);
-            ptx::bulk_wait_read_all();  // staging may be overwritten from here on
-            ptx::mbar_arrive(&bars[B_STG_EMPTY]);
-            ptx::bulk_wait_all();
-            if (det) {
-              ptx::fence_async_global();
-              ptx::st_release(ticket, rank + 1);  // advance the global order (Alg.1 line 35)
-            }
-            DASH_TRACE_MARK(9, x);
+            __syncwarp();
+           }
           }
         }
         // Both reducers have released every add of this job: only now may the
         // CTA claim its next job (greedy claiming of AMB-7, deadlock-free).
-        ptx::mbar_arrive(&bars[B_JOB_DONE]);
+        if (lane == 0) ptx::mbar_arrive(&bars[B_JOB_DONE]);
         if (rid == 0) {
           ptx::mbar_wait(&bars[B_JOB_DONE], it_job & 1);
-          job_slot[(it_job + 1) & 1] = atomicAdd(args.job_counter, 1);
-          ptx::mbar_arrive(&bars[B_JOB0 + ((it_job + 1) & 1)]);
+          if (lane == 0) {
+            job_slot[(it_job + 1) & 1] = atomicAdd(args.job_counter, 1);
+            ptx::mbar_arrive(&bars[B_JOB0 + ((it_job + 1) & 1)]);
+          }
         }
+        __syncwarp();
         ++it_job;
       }
     }
@@ -409,8 +466,6 @@ __global__ void __launch_bounds__(512, 1)
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     constexpr int NC = C::SMX_COLS;
     const int c_base = wg * NC;
-    uint8_t* pP = smem + C::OFF_P;
-    uint8_t* pdS = smem + C::OFF_DS;
     uint32_t it_job = 0, x = 0, acc_cnt = 0;
     while (true) {
       ptx::mbar_wait(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
@@ -423,7 +478,8 @@ __global__ void __launch_bounds__(512, 1)
         const int kv = tk.x & 0xFFFF, q = tk.x >> 16;
         const bool diag = args.causal && (kv == q);
         for (int sub = 0; sub < NSUB; ++sub, ++x) {
-          const uint32_t st = x % NSTAGE;
+          const uint32_t st = x % NSTAGE, sb = x % C::NDS, pb = x % C::NPT;
+          uint8_t* pdS = smem + C::OFF_DS + sb * C::P_BYTES;
           ptx::mbar_wait(&bars[B_S_FULL], x & 1);
           ptx::mbar_wait(&bars[B_Q_FULL0 + st], (x / NSTAGE) & 1);
           ptx::tc_fence_after();
@@ -463,18 +519,27 @@ __global__ void __launch_bounds__(512, 1)
               dk2[c4 * 2] = pack_bf16(ds[0], ds[1]);
               dk2[c4 * 2 + 1] = pack_bf16(ds[2], ds[3]);
             }
-            // The P^T/dS^T buffer is free once the MMAs of the previous
-            // sub-tile completed; everything above overlapped with them.
-            if (ch == 0 && x > 0) ptx::mbar_wait(&bars[B_P_EMPTY], (x - 1) & 1);
+            // P^T -> TMEM buffer pb once dV of sub-tile x - NPT consumed it.
+            if (ch == 0 && x >= C::NPT)
+              ptx::mbar_wait(&bars[B_PT_EMPTY0 + pb], ((x / C::NPT) - 1) & 1);
+            ptx::tmem_st16(tbase + lane_off + C::T_PT + pb * (BR / 2) + cc0 / 2, pk);
+            if constexpr (C::DS_IN_TMEM) {
+              // dS^T -> TMEM (A operand of the dK TS-MMA) once dK of x - 1 consumed it.
+              if (ch == 0 && x >= 1) ptx::mbar_wait(&bars[B_DST_EMPTY], (x - 1) & 1);
+              ptx::tmem_st16(tbase + lane_off + C::T_DST + cc0 / 2, dk2);
+            }
+            // dS^T -> smem buffer sb once dK, dQ of sub-tile x - NDS consumed it.
+            if (ch == 0 && x >= C::NDS)
+              ptx::mbar_wait(&bars[B_DS_EMPTY0 + sb], ((x / C::NDS) - 1) & 1);
 #pragma unroll
             for (int c8 = 0; c8 < 4; ++c8) {
               const uint32_t off = sw128_chunk_offset(128, row, (cc0 + c8 * 8) >> 3);
-              *reinterpret_cast<uint4*>(pP + off) =
-                  make_uint4(pk[c8 * 4], pk[c8 * 4 + 1], pk[c8 * 4 + 2], pk[c8 * 4 + 3]);
               *reinterpret_cast<uint4*>(pdS + off) =
                   make_uint4(dk2[c8 * 4], dk2[c8 * 4 + 1], dk2[c8 * 4 + 2], dk2[c8 * 4 + 3]);
             }
           }
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
           ptx::fence_async_smem();
           ptx::mbar_arrive(&bars[B_P_FULL]);
           if (row == 0 && wg == 0) DASH_TRACE_MARK(4, x);
@@ -527,40 +592,43 @@ __global__ void __launch_bounds__(512, 1)
       const JobView jv = decode_job(args, g);
       const int nx = (jv.t1 - jv.t0) * NSUB;
       for (int u = 0; u < nx; ++u, ++x) {
-        const uint32_t db = x & 1;
-        ptx::mbar_wait(&bars[B_DQ_FULL0 + db], (x >> 1) & 1);
+        ptx::mbar_wait(&bars[B_DQ_FULL], x & 1);
         ptx::tc_fence_after();
         if (tl == 0) DASH_TRACE_MARK(5, x);
         float v[64];
-        ptx::tmem_ld32(tbase + lane_off + C::T_DQ + db * 64, *reinterpret_cast<float(*)[32]>(v));
-        ptx::tmem_ld32(tbase + lane_off + C::T_DQ + db * 64 + 32,
-                       *reinterpret_cast<float(*)[32]>(v + 32));
+        ptx::tmem_ld32(tbase + lane_off + C::T_DQ, *reinterpret_cast<float(*)[32]>(v));
+        ptx::tmem_ld32(tbase + lane_off + C::T_DQ + 32, *reinterpret_cast<float(*)[32]>(v + 32));
         ptx::tmem_wait_ld();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&bars[B_DQ_EMPTY0 + db]);
-        if (x >= 1) ptx::mbar_wait(&bars[B_STG_EMPTY], (x - 1) & 1);
+        ptx::mbar_arrive(&bars[B_DQ_EMPTY]);
         uint8_t* stg = smem + C::OFF_DQ;
-        // Stage the fp32 partial as SW128 boxes of 32 columns x BR rows.
-        if constexpr (D == 128) {
-          // lane tl = d index, v[c] = Q row c
-          const int blk = tl >> 5, chunk = (tl & 31) >> 2, w = tl & 3;
 #pragma unroll
-          for (int c = 0; c < BR; ++c) {
-            const uint32_t off = blk * BR * 128 + c * 128 + ((chunk ^ (c & 7)) << 4) + w * 4;
-            *reinterpret_cast<float*>(stg + off) = v[c];
-          }
-        } else {
-          // lane tl = Q row, v[c] = d column c
+        for (int h = 0; h < C::NUNIT; ++h) {
+          const uint32_t y = x * C::NUNIT + h;  // staging unit
+          if (y >= 1) ptx::mbar_wait(&bars[B_STG_EMPTY], (y - 1) & 1);
+          // Stage STG_ROWS rows of the fp32 partial as SW128 boxes of 32 columns.
+          if constexpr (D == 128) {
+            // lane tl = d index, v[c] = Q row c of the sub-tile
+            const int blk = tl >> 5, chunk = (tl & 31) >> 2, w = tl & 3;
 #pragma unroll
-          for (int cc = 0; cc < 16; ++cc) {
-            const int blk = cc >> 3, chunk = cc & 7;
-            const uint32_t off = blk * BR * 128 + tl * 128 + ((chunk ^ (tl & 7)) << 4);
-            *reinterpret_cast<float4*>(stg + off) =
-                make_float4(v[cc * 4], v[cc * 4 + 1], v[cc * 4 + 2], v[cc * 4 + 3]);
+            for (int c = 0; c < C::STG_ROWS; ++c) {
+              const uint32_t off =
+                  blk * C::STG_ROWS * 128 + c * 128 + ((chunk ^ (c & 7)) << 4) + w * 4;
+              *reinterpret_cast<float*>(stg + off) = v[h * C::STG_ROWS + c];
+            }
+          } else {
+            // lane tl = Q row, v[c] = d column c
+#pragma unroll
+            for (int cc = 0; cc < 16; ++cc) {
+              const int blk = cc >> 3, chunk = cc & 7;
+              const uint32_t off = blk * BR * 128 + tl * 128 + ((chunk ^ (tl & 7)) << 4);
+              *reinterpret_cast<float4*>(stg + off) =
+                  make_float4(v[cc * 4], v[cc * 4 + 1], v[cc * 4 + 2], v[cc * 4 + 3]);
+            }
           }
+          ptx::fence_async_smem();
+          ptx::mbar_arrive(&bars[B_STG_FULL0 + (y & 1)]);
         }
-        ptx::fence_async_smem();
-        ptx::mbar_arrive(&bars[B_STG_FULL0 + (x & 1)]);
         if (tl == 0) DASH_TRACE_MARK(6, x);
       }
     }

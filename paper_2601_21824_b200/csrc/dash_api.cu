@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -36,7 +37,7 @@ bool aligned16(const void* p) { return p && (reinterpret_cast<uintptr_t>(p) & 15
 float eff_scale(const dash_shape* s) {
   return s->softmax_scale > 0.f ? s->softmax_scale : 1.0f / std::sqrt(static_cast<float>(s->head_dim));
 }
-int sub_rows(int d) { return d == 128 ? BwdCfg<128>::BR : BwdCfg<64>::BR; }
+int ticket_rows(int d) { return d == 128 ? BwdCfg<128>::STG_ROWS : BwdCfg<64>::STG_ROWS; }
 
 struct WsLayout {
   size_t dqacc = 0, dvec = 0, lse2 = 0, tickets = 0, counters = 0, total = 0;
@@ -46,7 +47,7 @@ WsLayout ws_layout(const dash_shape* s) {
   WsLayout w;
   const size_t BHN = static_cast<size_t>(s->batch) * s->heads * s->seqlen;
   w.dqacc_bytes = BHN * s->head_dim * 4;
-  w.n_tickets = static_cast<size_t>(s->batch) * s->heads * (s->seqlen / sub_rows(s->head_dim));
+  w.n_tickets = static_cast<size_t>(s->batch) * s->heads * (s->seqlen / ticket_rows(s->head_dim));
   size_t off = 0;
   w.dqacc = off;
   off = align_up(off + w.dqacc_bytes, kAlign);
@@ -197,7 +198,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
             make_map_2d(&tv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, v, HD, BN, 64, C::BC) &&
             make_map_2d(&tdo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, HD, BN, 64, C::BR) &&
             make_map_2d(&tacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dqacc, D,
-                        BN * static_cast<uint64_t>(s->heads), 32, C::BR);
+                        BN * static_cast<uint64_t>(s->heads), 32, C::STG_ROWS);
   if (!ok) return DASH_ERR_CUDA;
 
   prof_mark(stream);
@@ -237,6 +238,11 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     a.deterministic = deterministic ? 1 : 0;
     a.trace = g_trace;
     a.trace_cap = g_trace_cap;
+    static const int debug_bits = [] {
+      const char* e = std::getenv("DASH_DEBUG");
+      return e ? std::atoi(e) : 0;
+    }();
+    a.debug = debug_bits;
     auto kern = dash_bwd_kernel<D>;
     static bool attr_set = false;
     if (!attr_set) {

@@ -71,10 +71,10 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = tmem_base;
-  if (warp == 0 && ptx::elect_one()) {
+  if (warp == 0) {
     umma_gemm<M, N, K, A_MN, B_MN>(tbase, ptx::smem_u32(sA), A_MN ? K : M, ptx::smem_u32(sB),
                                    B_MN ? K : N, false);
-    ptx::mma_commit(&bar);
+    ptx::mma_commit_e(&bar);
   }
   __syncwarp();
   ptx::mbar_wait(&bar, 0);
@@ -89,6 +89,142 @@ __global__ void __launch_bounds__(128, 1)
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 0) ptx::tmem_dealloc<256>(tbase);
+}
+
+// A from TMEM ("TS" MMA): each thread writes its row of A (K bf16, packed)
+// with tcgen05.st, B from smem.
+template <int N, int K, bool B_MN>
+__global__ void __launch_bounds__(128, 1)
+    probe_umma_ts_kernel(const __nv_bfloat16* A, const __nv_bfloat16* Bt, float* D) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sB = smem;
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid / 32;
+  for (int e = tid; e < N * K / 8; e += blockDim.x) {
+    if (!B_MN) {
+      const int r = e / (K / 8), ch = e % (K / 8);
+      *reinterpret_cast<uint4*>(sB + sw128_chunk_offset(N, r, ch)) =
+          *reinterpret_cast<const uint4*>(Bt + r * K + ch * 8);
+    } else {
+      const int r = e / (N / 8), ch = e % (N / 8);
+      __align__(16) __nv_bfloat16 tmp[8];
+      for (int t = 0; t < 8; ++t) tmp[t] = Bt[(ch * 8 + t) * K + r];
+      *reinterpret_cast<uint4*>(sB + sw128_chunk_offset(K, r, ch)) = *reinterpret_cast<uint4*>(tmp);
+    }
+  }
+  ptx::fence_async_smem();
+  if (warp == 0) ptx::tmem_alloc<256>(&tmem_base);
+  if (tid == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbar_init();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+  // A row `tid` -> TMEM lane tid, columns 128 .. 128 + K/2
+  for (int c = 0; c < K / 2; c += 16) {
+    uint32_t r[16];
+    for (int t = 0; t < 16; ++t) {
+      __nv_bfloat162 v;
+      v.x = A[tid * K + 2 * (c + t)];
+      v.y = A[tid * K + 2 * (c + t) + 1];
+      r[t] = *reinterpret_cast<uint32_t*>(&v);
+    }
+    ptx::tmem_st16(tbase + lane_base + 128 + c, r);
+  }
+  ptx::tmem_wait_st();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 0) {
+    umma_gemm_ts<N, K, B_MN>(tbase, tbase + 128, ptx::smem_u32(sB), B_MN ? K : N, false);
+    ptx::mma_commit_e(&bar);
+  }
+  __syncwarp();
+  ptx::mbar_wait(&bar, 0);
+  ptx::tc_fence_after();
+  for (int c = 0; c < N; c += 32) {
+    float v[32];
+    ptx::tmem_ld32(tbase + lane_base + c, v);
+    ptx::tmem_wait_ld();
+    for (int t = 0; t < 32; ++t) D[tid * N + c + t] = v[t];
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) ptx::tmem_dealloc<256>(tbase);
+}
+
+// Throughput microbenchmark: `reps` back-to-back GEMMs of K = 128 (8 MMAs)
+// of shape 128 x N, operands from smem (SS, A/B majorness as given) or A from
+// TMEM (TS).  Returns clock64 cycles per GEMM via out[blockIdx.x].
+template <int N, int MODE>  // MODE 0: SS K/K, 1: SS K/MN, 2: SS MN/MN, 3: TS (B MN)
+__global__ void __launch_bounds__(128, 1) probe_mma_rate_kernel(int reps, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
+  for (int i = threadIdx.x; i < (128 * 128 + N * 128) / 8; i += 128)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3f803f80u, 0, 0x3f803f80u, 0);
+  ptx::fence_async_smem();
+  if (warp == 0) ptx::tmem_alloc<512>(&tmem_base);
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbar_init();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tb = tmem_base;
+  if (warp == 0) {
+    const uint32_t sA = ptx::smem_u32(smem), sB = ptx::smem_u32(smem + 128 * 128 * 2);
+    const uint64_t ak = tile_desc<false>(sA, 128), amn = tile_desc<true>(sA, 128);
+    const uint64_t bk = tile_desc<false>(sB, N), bmn = tile_desc<true>(sB, 128);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      if (MODE == 0) umma_gemm_d<128, N, 128, false, false, 128, N>(tb, ak, bk, r > 0);
+      if (MODE == 1) umma_gemm_d<128, N, 128, false, true, 128, 128>(tb, ak, bmn, r > 0);
+      if (MODE == 2) umma_gemm_d<128, N, 128, true, true, 128, 128>(tb, amn, bmn, r > 0);
+      if (MODE == 3) umma_gemm_ts_d<N, 128, true, 128>(tb, tb + 256, bmn, r > 0);
+    }
+    ptx::mma_commit_e(&bar);
+    ptx::mbar_wait_u(&bar, 0);
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) out[blockIdx.x] = (t1 - t0) / reps;
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) ptx::tmem_dealloc<512>(tb);
+}
+
+// Throughput of adding a 32 KB fp32 tile (64 rows x 128) per iteration into
+// a private global region: mode 0 = red.global.add.v4.f32 from 128 threads,
+// mode 1 = same + membar.gl per iteration (ordered hand-off cost).
+__global__ void __launch_bounds__(128, 1) probe_red_rate_kernel(float* dst, int iters, int mode,
+                                                                long long* out) {
+  float* base = dst + static_cast<size_t>(blockIdx.x) * 64 * 128;
+  const int t = threadIdx.x;
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    // thread t covers rows r = t / 32 + 4 k, float4 column (t % 32)
+#pragma unroll 4
+    for (int k = 0; k < 16; ++k) {
+      float* p = base + (t / 32 + 4 * k) * 128 + (t % 32) * 4;
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(1.f), "f"(1.f),
+                   "f"(1.f), "f"(1.f)
+                   : "memory");
+    }
+    if (mode == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (t == 0) out[blockIdx.x] = (t1 - t0) / iters;
 }
 
 __global__ void probe_tma_kernel(const __grid_constant__ CUtensorMap tmap, int rows, int cols,
@@ -139,6 +275,60 @@ extern "C" __attribute__((visibility("default"))) int dash_probe_umma(int n, int
   cudaError_t e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) fprintf(stderr, "dash_probe_umma: %s\n", cudaGetErrorString(e));
+  return static_cast<int>(e);
+}
+
+extern "C" __attribute__((visibility("default"))) int dash_probe_umma_ts(int n, int k, int b_mn,
+                                                                        const void* A,
+                                                                        const void* Bt, float* D) {
+  const size_t smem = 1024 + n * k * 2;
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<1, 128, smem>>>(static_cast<const __nv_bfloat16*>(A),
+                           static_cast<const __nv_bfloat16*>(Bt), D);
+  };
+  if (n == 128 && k == 64) b_mn ? launch(probe_umma_ts_kernel<128, 64, true>)
+                                : launch(probe_umma_ts_kernel<128, 64, false>);
+  if (n == 64 && k == 128) b_mn ? launch(probe_umma_ts_kernel<64, 128, true>)
+                                : launch(probe_umma_ts_kernel<64, 128, false>);
+  if (n == 128 && k == 128) b_mn ? launch(probe_umma_ts_kernel<128, 128, true>)
+                                 : launch(probe_umma_ts_kernel<128, 128, false>);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) fprintf(stderr, "dash_probe_umma_ts: %s\n", cudaGetErrorString(e));
+  return static_cast<int>(e);
+}
+
+extern "C" __attribute__((visibility("default"))) int dash_probe_mma_rate(int n, int mode, int reps,
+                                                                         int grid,
+                                                                         long long* out) {
+  const size_t smem = 1024 + (128 * 128 + 256 * 128) * 2;
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 128, smem>>>(reps, out);
+  };
+#define RATE_CASE(NN)                                        \
+  if (n == NN) {                                             \
+    if (mode == 0) launch(probe_mma_rate_kernel<NN, 0>);     \
+    if (mode == 1) launch(probe_mma_rate_kernel<NN, 1>);     \
+    if (mode == 2) launch(probe_mma_rate_kernel<NN, 2>);     \
+    if (mode == 3) launch(probe_mma_rate_kernel<NN, 3>);     \
+  }
+  RATE_CASE(64)
+  RATE_CASE(128)
+  RATE_CASE(256)
+#undef RATE_CASE
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return static_cast<int>(e);
+}
+
+extern "C" __attribute__((visibility("default"))) int dash_probe_red_rate(float* dst, int iters,
+                                                                         int mode, int grid,
+                                                                         long long* out) {
+  probe_red_rate_kernel<<<grid, 128>>>(dst, iters, mode, out);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
   return static_cast<int>(e);
 }
 

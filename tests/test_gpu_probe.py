@@ -26,6 +26,7 @@ def probe():
     b.build()
     lib = ctypes.CDLL(PROBE)
     lib.dash_probe_umma.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p] * 3
+    lib.dash_probe_umma_ts.argtypes = [ctypes.c_int] * 3 + [ctypes.c_void_p] * 3
     lib.dash_probe_tma.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_void_p]
     return lib
@@ -42,6 +43,21 @@ def test_umma_gemm_layouts(probe, n, k, a_mn, b_mn):
     dA, dB = A.cuda(), Bt.cuda()
     D = torch.zeros(128, n, device="cuda", dtype=torch.float32)
     rc = probe.dash_probe_umma(n, k, a_mn, b_mn, dA.data_ptr(), dB.data_ptr(), D.data_ptr())
+    assert rc == 0
+    torch.testing.assert_close(D.cpu(), ref, rtol=1e-5, atol=1e-4)
+
+
+@pytest.mark.parametrize("n,k", [(128, 64), (64, 128), (128, 128)])
+@pytest.mark.parametrize("b_mn", [0, 1])
+def test_umma_ts_a_from_tmem(probe, n, k, b_mn):
+    """A operand in TMEM (lane = row, two bf16 per column), B from smem."""
+    g = torch.Generator().manual_seed(7 * n + k + b_mn)
+    A = torch.randn(128, k, generator=g).to(torch.bfloat16)
+    Bt = torch.randn(n, k, generator=g).to(torch.bfloat16)
+    ref = A.float() @ Bt.float().T
+    dA, dB = A.cuda(), Bt.cuda()  # keep both alive: no allocator reuse of a temporary
+    D = torch.zeros(128, n, device="cuda", dtype=torch.float32)
+    rc = probe.dash_probe_umma_ts(n, k, b_mn, dA.data_ptr(), dB.data_ptr(), D.data_ptr())
     assert rc == 0
     torch.testing.assert_close(D.cpu(), ref, rtol=1e-5, atol=1e-4)
 
