@@ -395,9 +395,11 @@ __global__ void __launch_bounds__(512, 1)
             int* ticket = args.tickets + static_cast<size_t>(jv.bh) * n_units + urow / C::STG_ROWS;
             if (det) {
               // Wait until the global order grants this block its turn (Alg.1 line 33).
+              // Spin with relaxed loads (an acquire per poll would invalidate L1
+              // every iteration); one acquire once the turn has come.
               if (ptx::ld_acquire(ticket) != rank) {
                 const long long t_start = clock64();
-                while (ptx::ld_acquire(ticket) != rank) {
+                while (ptx::ld_relaxed(ticket) != rank) {
                   __nanosleep(32);
                   if (clock64() - t_start > 8 * ptx::kWatchdogCycles ||
                       *reinterpret_cast<volatile int*>(&ptx::g_dash_abort)) {  // ~35 s bound
@@ -408,6 +410,7 @@ __global__ void __launch_bounds__(512, 1)
                     break;
                   }
                 }
+                (void)ptx::ld_acquire(ticket);
               }
             }
             // Order the ticket acquire (generic proxy) before the reduce (async
@@ -434,10 +437,17 @@ __global__ void __launch_bounds__(512, 1)
               if (h == 0) DASH_TRACE_MARK(8, x / C::NUNIT);
               ptx::bulk_wait_read_all();  // staging may be overwritten from here on
               ptx::mbar_arrive(&bars[B_STG_EMPTY]);
+              if (h == 0) DASH_TRACE_MARK(11, x / C::NUNIT);
               ptx::bulk_wait_all();
+              if (h == 0) DASH_TRACE_MARK(12, x / C::NUNIT);
               if (det) {
+                // Advance the global order (Alg.1 line 35): proxy fence (the
+                // reduce wrote through the async proxy) + gpu-scope release.
+                // Measured: a relaxed store here is NOT safe -- completion of
+                // the bulk group alone does not order the reduce's writes
+                // before the flag (tests/test_gpu_bwd.py catches it).
                 ptx::fence_async_global();
-                ptx::st_release(ticket, rank + 1);  // advance the global order (Alg.1 line 35)
+                ptx::st_release(ticket, rank + 1);
               }
               if (h == C::NUNIT - 1) DASH_TRACE_MARK(9, x / C::NUNIT);
             }

@@ -177,7 +177,12 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
   if (cudaGetDevice(&dev) != cudaSuccess) return DASH_ERR_CUDA;
   const int sms = device_sms(dev);
   const int total_jobs = tab->jobs * s->batch * s->heads;
-  const int grid = total_jobs < sms ? total_jobs : sms;
+  int grid = total_jobs < sms ? total_jobs : sms;
+  static const int debug_bits = [] {
+    const char* e = std::getenv("DASH_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+
   if (schedule == kShift && tab->jobs > grid) return DASH_ERR_UNSUPPORTED;
   const DevTable* dt = device_table(dev, tab);
   if (!dt) return DASH_ERR_CUDA;
@@ -238,10 +243,6 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     a.deterministic = deterministic ? 1 : 0;
     a.trace = g_trace;
     a.trace_cap = g_trace_cap;
-    static const int debug_bits = [] {
-      const char* e = std::getenv("DASH_DEBUG");
-      return e ? std::atoi(e) : 0;
-    }();
     a.debug = debug_bits;
     auto kern = dash_bwd_kernel<D>;
     static bool attr_set = false;

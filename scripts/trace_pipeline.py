@@ -18,7 +18,7 @@ from paper_2601_21824_b200 import dash  # noqa: E402
 from paper_2601_21824_b200.inputs import attn_inputs, sweep_shape  # noqa: E402
 
 SLOTS = ["sdp_issue", "p_seen", "dq_issue", "smx_start", "smx_done", "drain_start", "staged",
-         "acquired", "reduce_issued", "released", "load_issued"]
+         "acquired", "reduce_issued", "released", "load_issued", "read_done", "write_done"]
 
 
 def main():
@@ -48,7 +48,10 @@ def main():
         nx = int(np.count_nonzero(t[cta, :, 0]))
         if nx < 2:
             continue
-        a = t[cta, :nx, :11]
+        a = t[cta, :nx, :13]
+        per.setdefault("reduce_read", []).extend((a[:, 11] - a[:, 8]).tolist())
+        per.setdefault("reduce_write", []).extend((a[:, 12] - a[:, 11]).tolist())
+        per.setdefault("write_to_release", []).extend((a[:, 9] - a[:, 12]).tolist())
         per.setdefault("load_to_sdp_issue", []).extend((a[:, 0] - a[:, 10]).tolist())
         per.setdefault("period", []).extend(np.diff(a[:, 0]).tolist())
         per.setdefault("mma_wait_p", []).extend((a[:, 1] - a[:, 0]).tolist())
@@ -66,9 +69,9 @@ def main():
         res[k] = {"p10": float(np.percentile(v, 10)), "p50": float(np.median(v)),
                   "p90": float(np.percentile(v, 90)), "mean": float(v.mean())}
     # raw stamps of CTA 0's first sub-tiles, relative to its first S/dP issue
-    a0 = t[0, :24, :11]
+    a0 = t[0, :24, :13]
     base = a0[0, 0]
-    res["raw_cta0"] = {SLOTS[i]: [int(v - base) if v else None for v in a0[:, i]] for i in range(11)}
+    res["raw_cta0"] = {SLOTS[i]: [int(v - base) if v else None for v in a0[:, i]] for i in range(13)}
     print(json.dumps({k: v for k, v in res.items() if k != "raw_cta0"}, indent=1))
     if args.out:
         with open(args.out, "w") as f:
