@@ -227,6 +227,35 @@ __global__ void __launch_bounds__(128, 1) probe_red_rate_kernel(float* dst, int 
   if (t == 0) out[blockIdx.x] = (t1 - t0) / iters;
 }
 
+// TMA load latency: each CTA repeatedly loads two 64-col x `rows` bf16 boxes
+// (a Q sub-tile of [B,N,H,d] at d = 128) into smem and waits; returns the mean
+// cycles from issue to mbarrier completion in out[blockIdx.x].
+__global__ void probe_tma_latency_kernel(const __grid_constant__ CUtensorMap tmap, int rows,
+                                         int iters, int row_stride_tiles, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  long long total = 0;
+  if (threadIdx.x == 0) {
+    for (int it = 0; it < iters; ++it) {
+      const int r0 = ((blockIdx.x * 7 + it) % row_stride_tiles) * rows;
+      const long long t0 = clock64();
+      ptx::mbar_arrive_expect_tx(&bar, 2 * rows * 128);
+      ptx::tma_load_2d(smem, &tmap, &bar, 0, r0);
+      ptx::tma_load_2d(smem + rows * 128, &tmap, &bar, 64, r0);
+      ptx::mbar_wait(&bar, it & 1);
+      total += clock64() - t0;
+    }
+    out[blockIdx.x] = total / iters;
+  }
+}
+
 __global__ void probe_tma_kernel(const __grid_constant__ CUtensorMap tmap, int rows, int cols,
                                  uint8_t* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -327,6 +356,31 @@ extern "C" __attribute__((visibility("default"))) int dash_probe_red_rate(float*
                                                                          int mode, int grid,
                                                                          long long* out) {
   probe_red_rate_kernel<<<grid, 128>>>(dst, iters, mode, out);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return static_cast<int>(e);
+}
+
+extern "C" __attribute__((visibility("default"))) int dash_probe_tma_latency(
+    const void* src, int total_rows, int ld_elems, int rows, int iters, int grid, long long* out) {
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  cudaDriverEntryPointQueryResult qres;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode),
+                          cudaEnableDefault, &qres);
+  if (!encode) return -1;
+  CUtensorMap tmap;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(ld_elems), static_cast<cuuint64_t>(total_rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_elems) * 2};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(rows)};
+  cuuint32_t estr[2] = {1, 1};
+  if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(src), dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -2;
+  const size_t smem = 1024 + 2 * rows * 128;
+  cudaFuncSetAttribute(probe_tma_latency_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  probe_tma_latency_kernel<<<grid, 32, smem>>>(tmap, rows, iters, total_rows / rows, out);
   cudaError_t e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = cudaGetLastError();
   return static_cast<int>(e);
