@@ -57,6 +57,13 @@ def _load():
     lib.dash_attn_bwd_trace.restype = st
     lib.dash_attn_bwd_trace.argtypes = [SP, vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp, sz,
                                         vp, i, vp]
+    lib.dash_attn_bwd_tile_rows.restype = i
+    lib.dash_attn_bwd_tile_rows.argtypes = [SP, i, i]
+    lib.dash_attn_bwd_dump_bytes.restype = sz
+    lib.dash_attn_bwd_dump_bytes.argtypes = [SP]
+    lib.dash_attn_bwd_dump.restype = st
+    lib.dash_attn_bwd_dump.argtypes = [SP, vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp, sz,
+                                       vp, sz, vp]
     lib.dash_attn_bwd_host_workspace_bytes.restype = sz
     lib.dash_attn_bwd_host_workspace_bytes.argtypes = [SP, i, i, i]
     lib.dash_attn_bwd_host.restype = st
@@ -174,6 +181,33 @@ def attn_bwd_trace(q, k, v, o, dout, lse, causal: bool, schedule, deterministic,
                                     workspace.numel(), _ptr(trace), trace_cap, _stream(q)),
            "dash_attn_bwd_trace")
     return (dq, dk, dv), trace
+
+
+def tile_rows(shape_bnhd, causal: bool, schedule) -> int:
+    """dash_attn_bwd_tile_rows: 256 (2-CTA pair tiles) or 128."""
+    B, N, H, d = shape_bnhd
+    shp = Shape(B, N, H, d, 0.0)
+    return int(_lib.dash_attn_bwd_tile_rows(ctypes.byref(shp), int(causal), _sched(schedule)))
+
+
+def attn_bwd_dump(q, k, v, o, dout, lse, causal: bool, schedule, deterministic=True, scale=None,
+                  workspace=None, out=None):
+    """dash_attn_bwd_dump: returns ((dq, dk, dv), partials [B*H, n, N, d] fp32 on device, workspace)."""
+    sched = _sched(schedule)
+    if workspace is None:
+        workspace = alloc_workspace(q.shape, causal, sched, deterministic, q.device)
+    dq, dk, dv = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)) if out is None else out
+    B, N, H, d = q.shape
+    shp = _shape(q, scale)
+    nbytes = int(_lib.dash_attn_bwd_dump_bytes(ctypes.byref(shp)))
+    parts = torch.zeros((B * H, N // 128, N, d), dtype=torch.float32, device=q.device)
+    assert parts.numel() * 4 == nbytes
+    _check(_lib.dash_attn_bwd_dump(ctypes.byref(shp), _ptr(q), _ptr(k), _ptr(v), _ptr(o),
+                                   _ptr(dout), _ptr(lse), _ptr(dq), _ptr(dk), _ptr(dv),
+                                   int(causal), sched, int(deterministic), _ptr(workspace),
+                                   workspace.numel(), _ptr(parts), nbytes, _stream(q)),
+           "dash_attn_bwd_dump")
+    return (dq, dk, dv), parts, workspace
 
 
 def host_workspace_bytes(shape_bnhd, causal: bool, schedule=NAIVE, deterministic=True) -> int:

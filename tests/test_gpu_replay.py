@@ -1,0 +1,110 @@
+"""T5 replay (SURVEY.md §8(c) c4 "GPU exact order"): the ordered dQ reduction
+is pinned bit for bit, not just to a tolerance.
+
+dash_attn_bwd_dump hands back every dQ partial dQ_local = dS K_i (Alg.1 line
+28) exactly as it entered the reduction.  The host then re-sums each
+dQ tile's partials in the order the paper prescribes -- the ranks come from
+oracle/dag_oracle.reduction_ranks, built from the paper's schedule
+definitions (AMB-6), not from the product's tables --
+with one IEEE fp32 round-to-nearest add per contribution (Alg.1 line 34,
+P:396), then applies dq = bf16_rn(scale * sum) (AMB-14).  The GPU's fp32
+accumulator and its dq must match those bits exactly.  A wrong rank,
+a skipped or doubled contribution, an add that raced its predecessor, or a
+scale applied per partial all change bits.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import dag_oracle as dag
+from paper_2601_21824_b200.inputs import attn_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dash():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2601_21824_b200 import build
+    build.build()
+    from paper_2601_21824_b200 import dash as d
+    return d
+
+
+def bf16_rn_bits(x32: np.ndarray) -> np.ndarray:
+    """IEEE binary32 -> bfloat16 bit pattern, round to nearest even (finite inputs)."""
+    u = x32.astype(np.float32).view(np.uint32).astype(np.uint64)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+@pytest.mark.parametrize("N", [512, 384])
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("schedule", ["naive", "descending", "shift"])
+def test_dq_equals_host_resum_in_paper_order(dash, N, d, causal, schedule):
+    B, H = 1, 2
+    T = dash.tile_rows((B, N, H, d), causal, schedule)   # 256: 2-CTA pair tiles (AMB-26)
+    n = N // T
+    if schedule == "shift" and causal and n % 2:
+        pytest.skip("Symmetric Shift needs an even number of KV tiles (AMB-10)")
+    mask = dag.CAUSAL if causal else dag.FULL
+    sched = {"naive": dag.NAIVE, "descending": dag.DESCENDING, "shift": dag.SHIFT}[schedule]
+    g = {k: v.cuda() for k, v in attn_inputs(B, N, H, d, seed=7).items()}
+    o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], causal)
+    (dq, _, _), parts, ws = dash.attn_bwd_dump(g["q"], g["k"], g["v"], o, g["do"], lse, causal,
+                                               schedule, True)
+    torch.cuda.synchronize()
+    parts = parts.cpu().numpy()                                        # [B*H, N/128, N, d] fp32
+    acc_gpu = ws[: B * H * N * d * 4].view(torch.float32).cpu().numpy().reshape(B * H, N, d)
+    dq_bits = dq.view(torch.int16).cpu().numpy().view(np.uint16)     # [B, N, H, d]
+    scale = np.float32(1.0) / np.sqrt(np.float32(d))
+    rank = dag.reduction_ranks(sched, n, mask)
+
+    def contribution(bh, i, j):
+        """KV tile i's partial for Q tile j, as it enters the ordered reduction."""
+        rows = slice(j * T, (j + 1) * T)
+        if T == 128:
+            return parts[bh, i, rows]
+        p0, p1 = parts[bh, 2 * i, rows], parts[bh, 2 * i + 1, rows]
+        c = (p0 + p1).astype(np.float32)       # CTA 0's partial + CTA 1's, in that order
+        if causal and i == j:
+            c[:128] = p0[:128]                 # keys of CTA 1 all masked: p0 alone
+        return c
+
+    checked_acc = 0
+    for bh in range(B * H):
+        b, h = divmod(bh, H)
+        for j in range(n):
+            order = sorted((rk, i) for (i, jj), rk in rank.items() if jj == j)
+            assert [rk for rk, _ in order] == list(range(len(order)))
+            rows = slice(j * T, (j + 1) * T)
+            acc = contribution(bh, order[0][1], j).copy()     # rank 0 stores
+            for _, i in order[1:]:                             # ranks 1.. add, in order
+                acc = (acc + contribution(bh, i, j)).astype(np.float32)
+            np.testing.assert_array_equal(acc_gpu[bh, rows].view(np.uint32), acc.view(np.uint32),
+                                          err_msg=f"dQacc bh={bh} tile={j}")
+            checked_acc += len(order) >= 2
+            want = bf16_rn_bits((acc * scale).astype(np.float32))
+            got = dq_bits[b, rows, h, :]
+            bad = np.count_nonzero(got != want)
+            assert bad == 0, f"dq bh={bh} tile={j}: {bad} of {want.size} bf16 values differ"
+    assert checked_acc > 0
+
+
+def test_partials_cover_exactly_the_visited_tiles(dash):
+    """Every (128-row KV block, 128-row Q block) pair the mask admits hands a
+    partial to the reduction, and no other: rows a block never visits stay
+    zero (holds for 128- and 256-row schedule tiles alike)."""
+    B, N, H, d = 1, 512, 1, 128
+    g = {k: v.cuda() for k, v in attn_inputs(B, N, H, d, seed=3).items()}
+    o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], True)
+    _, parts, _ = dash.attn_bwd_dump(g["q"], g["k"], g["v"], o, g["do"], lse, True, "shift", True)
+    parts = parts.cpu().numpy()[0]
+    for i in range(N // 128):
+        for j in range(N // 128):
+            blk = parts[i, j * 128:(j + 1) * 128]
+            if j >= i:
+                assert np.count_nonzero(blk) > blk.size // 2, (i, j)
+            else:
+                assert not np.any(blk), (i, j)
