@@ -187,24 +187,13 @@ dash_status dash_attn_bwd_trace(const dash_shape* shape, const void* q, const vo
                                 int deterministic, void* workspace, size_t workspace_bytes,
                                 unsigned long long* trace, int trace_cap, void* stream);
 
-/* Rows of the schedule's KV / Q tile that dash_attn_bwd uses for this
- * problem: 256 when N is a multiple of 256 (a cluster of two CTAs, 128 KV rows
- * each, runs one 256-row KV tile of the schedule and makes one ordered dQ add
- * per 256 x 256 task, AMB-26), else 128 (one CTA per 128-row tile).  Symmetric
- * Shift with an odd number of 256-row tiles uses 128.  The schedule (its Q
- * orders and reduction ranks) is the paper's over n = N / tile_rows tiles.
- * Returns 0 for an invalid shape. */
-int dash_attn_bwd_tile_rows(const dash_shape* shape, int causal, int schedule);
-
 /* Verification variant of dash_attn_bwd (same arguments and results) that
  * also writes every dQ partial dQ_local = dS K_i (Alg.1 line 28; fp32,
  * unscaled) as it is handed to the ordered reduction: partials is device
- * memory, fp32 [B*H][n][N][d] with n = N/128 128-row KV blocks, element
- * [bh][i][r][c] = the partial of KV rows [128 i, 128 i + 128) for query row r
- * (rows a block does not visit are left untouched; zero-fill first).  With
- * 256-row tiles (dash_attn_bwd_tile_rows) the contribution of KV tile p to
- * the ordered reduction is fp32(partial[2p] + partial[2p+1]) (block 2p+1
- * absent where all its keys are masked).  With the schedule's ranks this lets
+ * memory, fp32 [B*H][n][N][d] with n = N/128 KV tiles, element
+ * [bh][i][r][c] = the partial of KV tile i for query row r (rows of Q tiles
+ * that KV tile i does not visit are left untouched; zero-fill first).  With
+ * the schedule's ranks this lets
  * a test re-sum the partials in the paper's order on the host and compare dq
  * bit for bit (SURVEY.md §8(c) c4 "T5
  * replay").  partial_bytes must be >= dash_attn_bwd_dump_bytes(shape) (else

@@ -54,9 +54,8 @@ struct BwdArgs {
   unsigned long long* trace;  // optional clock64 trace [grid][trace_cap][16] (measurement only)
   int trace_cap;
   int debug;  // timing experiments only (env DASH_DEBUG): bit 0 skips the dQ reduce ops,
-             // bit 2 skips the dQ staging (with bit 0: the compute pipeline alone),
-             // bit 3 defers dQ(x) behind the next S/dP (MMA order experiment)
-  float* dump;           // verification only: every dQ partial, [B*H][N/128][N][d] fp32
+             // bit 2 skips the dQ staging (with bit 0: the compute pipeline alone)
+  float* dump;  // verification only: every dQ partial, [B*H][N/128][N][d] fp32
 };
 
 // Per-(CTA, sub-tile) clock64 stamps for pipeline analysis; a null trace
@@ -86,7 +85,6 @@ struct BwdCfg {
   // buffer was slower -- the softmax then waits on the dQ MMA.)
   static constexpr int STG_ROWS = BR;
   static constexpr int NUNIT = BR / STG_ROWS;  // staging units per sub-tile
-  static_assert(NUNIT == 1, "the drain stages one unit per sub-tile");
   static constexpr uint32_t DQ_BYTES = STG_ROWS * D * 4;
   static constexpr uint32_t OFF_K = 0;
   static constexpr uint32_t OFF_V = OFF_K + KV_BYTES;
@@ -138,9 +136,7 @@ enum : int {
   B_STG_FULL0 = 16, B_STG_FULL1 = 17,  // staging written, for reducer x & 1 (128)
   B_Q_FULL0 = 18,                      // + stage (<= 4): Q/dO/L/D loaded (tx)
   B_Q_EMPTY0 = 26,                     // + stage (<= 4): stage consumed (commit)
-  B_PEER_FULL = 30,                    // PAIR, CTA 0: CTA 1's partial staged (remote arrive)
-  B_PEER_EMPTY = 31,                   // PAIR, CTA 1: CTA 0 has read it (remote arrive)
-  B_COUNT = 32
+  B_COUNT = 30
 };
 
 __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, int c0, int c1) {
@@ -183,23 +179,13 @@ __device__ __forceinline__ JobView decode_job(const BwdArgs& a, int g) {
   return j;
 }
 
-// PAIR = false: one CTA per job KV tile (128 rows; the schedule model's tile).
-// PAIR = true : a cluster of two CTAs per job KV tile of 256 rows, each CTA
-// owning 128 of them (its own TMEM accumulators and 1-CTA MMAs).  Both CTAs
-// walk the same Q tiles (256 rows) in lockstep; CTA 1 hands its fp32 dQ
-// partial to CTA 0 through distributed shared memory, CTA 0 adds it to its
-// own (p0 + p1, fixed order) and makes the single ordered reduction of the
-// pair.  That halves the ordered adds, the reduce traffic into L2 and the
-// length of every dQ tile's ticket chain per FLOP (AMB-26).
-template <int D, bool PAIR>
+template <int D>
 __global__ void __launch_bounds__(512, 1)
     dash_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_dqacc, const BwdArgs args) {
   using C = BwdCfg<D>;
-  constexpr int BR = C::BR, NSTAGE = C::NSTAGE;
-  constexpr int QT = PAIR ? 256 : 128;  // schedule tile rows (KV tile of the job, Q tile)
-  constexpr int NSUB = QT / BR;         // Q sub-tiles per schedule Q tile
+  constexpr int BR = C::BR, NSUB = C::NSUB, NSTAGE = C::NSTAGE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t pad = (1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023;
   if (pad > C::SLACK) __trap();
@@ -214,16 +200,6 @@ __global__ void __launch_bounds__(512, 1)
   // Provably warp-uniform warp index (shfl broadcast): lets ptxas keep role
   // branches and everything derived from uniform values in uniform registers.
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  const int crank = PAIR ? static_cast<int>(ptx::cluster_ctarank()) : 0;
-  const int peer = crank ^ 1;
-  // Is Q sub-tile `sub` of Q tile q visible to any KV row that CTA r of the
-  // job's KV tile kv owns?  Only CTA 1 of a pair on a causal diagonal tile
-  // has wholly masked sub-tiles; every role skips them identically.
-  auto live_r = [&](int kv, int q, int sub, int r) -> bool {
-    if (!PAIR || !args.causal || r == 0) return true;
-    return q * QT + sub * BR + BR - 1 >= kv * QT + 128;
-  };
-  auto live = [&](int kv, int q, int sub) -> bool { return live_r(kv, q, sub, crank); };
 
   if (tid == 0) {
     for (int i = 0; i < B_COUNT; ++i) ptx::mbar_init(&bars[i], 1);
@@ -246,7 +222,6 @@ __global__ void __launch_bounds__(512, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  if constexpr (PAIR) ptx::cluster_sync();  // peer barriers initialised before any remote arrive
   const uint32_t tbase = *tmem_slot;
 
   const int n_units = args.N / C::STG_ROWS;  // tickets per head (one per staging unit)
@@ -256,7 +231,7 @@ __global__ void __launch_bounds__(512, 1)
     {  // whole warp converged; elect.sync issues
       uint32_t it_job = 0, kv_cnt = 0, q_cnt = 0;
       while (true) {
-        ptx::mbar_wait_u_cl(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
+        ptx::mbar_wait_u(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
         const int g = __shfl_sync(0xffffffffu, job_slot[it_job & 1], 0);
         ++it_job;
         if (g >= args.total_jobs || __shfl_sync(0xffffffffu, ptx::aborted(), 0)) break;
@@ -268,26 +243,24 @@ __global__ void __launch_bounds__(512, 1)
           if (kv != prev_kv) {
             if (kv_cnt > 0) ptx::mbar_wait_u(&bars[B_KV_EMPTY], (kv_cnt - 1) & 1);
             ptx::mbar_arrive_expect_tx_e(&bars[B_KV_FULL], 2 * C::KV_BYTES);
-            const int krow = jv.b * args.N + kv * QT + crank * 128;
 #pragma unroll
             for (int blk = 0; blk < D / 64; ++blk) {
               ptx::tma_load_2d_e(smem + C::OFF_K + blk * C::BC * 128, &tm_k, &bars[B_KV_FULL],
-                               jv.h * D + blk * 64, krow);
+                               jv.h * D + blk * 64, jv.b * args.N + kv * 128);
               ptx::tma_load_2d_e(smem + C::OFF_V + blk * C::BC * 128, &tm_v, &bars[B_KV_FULL],
-                               jv.h * D + blk * 64, krow);
+                               jv.h * D + blk * 64, jv.b * args.N + kv * 128);
             }
             ++kv_cnt;
             prev_kv = kv;
           }
           for (int sub = 0; sub < NSUB; ++sub) {
-            if (!live(kv, q, sub)) continue;
             const int stage = q_cnt % NSTAGE;
             if (q_cnt >= NSTAGE)
               ptx::mbar_wait_u(&bars[B_Q_EMPTY0 + stage], ((q_cnt / NSTAGE) - 1) & 1);
             uint64_t* full = &bars[B_Q_FULL0 + stage];
             if (lane == 0) DASH_TRACE_MARK(10, q_cnt);
             ptx::mbar_arrive_expect_tx_e(full, 2 * C::Q_BYTES + 2 * BR * 4);
-            const int row0 = q * QT + sub * BR;
+            const int row0 = q * 128 + sub * BR;
 #pragma unroll
             for (int blk = 0; blk < D / 64; ++blk) {
               ptx::tma_load_2d_e(smem + C::OFF_Q + stage * C::Q_BYTES + blk * BR * 128, &tm_q, full,
@@ -332,31 +305,8 @@ __global__ void __launch_bounds__(512, 1)
                                                        false);
         ptx::mma_commit_e(&bars[B_S_FULL]);
       };
-      // dQ_local of sub-tile y (Alg.1 line 28) into the single TMEM dQ
-      // buffer, once the drain has emptied it (partial of y - 1).
-      auto issue_dq = [&](uint32_t y) {
-        const uint32_t sby = y % C::NDS;
-        if (y >= 1) {
-          ptx::mbar_wait_u(&bars[B_DQ_EMPTY], (y - 1) & 1);
-          ptx::tc_fence_after();
-        }
-        if constexpr (D == 128) {
-          umma_gemm_d<128, BR, 128, true, true, 128, 128>(tbase + C::T_DQ, dK_mn,
-                                                          ddS_mn + sby * DS_STEP, false);
-        } else {
-          umma_gemm_d<128, D, 128, true, true, 128, 128>(tbase + C::T_DQ, ddS_mn + sby * DS_STEP,
-                                                         dK_mn, false);
-        }
-        if (lane == 0) DASH_TRACE_MARK(2, y);
-        ptx::mma_commit_e(&bars[B_DQ_FULL]);
-        ptx::mma_commit_e(&bars[B_DS_EMPTY0 + sby]);
-      };
-      // Issue order per sub-tile x: S/dP(x+1), [P(x)] dV(x), dK(x), dQ(x).
-      // Debug bit 3 defers dQ(x) behind S/dP(x+2) instead (measured: no
-      // difference, scripts/exp_reduce_path.py).
-      const bool defer_dq = (args.debug & 8) != 0;
       while (true) {
-        ptx::mbar_wait_u_cl(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
+        ptx::mbar_wait_u(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
         const int g = __shfl_sync(0xffffffffu, job_slot[it_job & 1], 0);
         ++it_job;
         if (g >= args.total_jobs || __shfl_sync(0xffffffffu, ptx::aborted(), 0)) break;
@@ -366,14 +316,9 @@ __global__ void __launch_bounds__(512, 1)
         while (ts < t1) {
           const int kv = args.tasks[ts].x & 0xFFFF;
           int te = ts + 1;
-          uint32_t nlive = 0;
-          for (int sub = 0; sub < NSUB; ++sub) nlive += live(kv, args.tasks[ts].x >> 16, sub);
-          while (te < t1 && (args.tasks[te].x & 0xFFFF) == kv) {
-            for (int sub = 0; sub < NSUB; ++sub) nlive += live(kv, args.tasks[te].x >> 16, sub);
-            ++te;
-          }
+          while (te < t1 && (args.tasks[te].x & 0xFFFF) == kv) ++te;
           te = __shfl_sync(0xffffffffu, te, 0);
-          const uint32_t nsub = __shfl_sync(0xffffffffu, nlive, 0);
+          const uint32_t nsub = static_cast<uint32_t>(te - ts) * NSUB;
           ptx::mbar_wait_u(&bars[B_KV_FULL], kv_cnt & 1);
           ++kv_cnt;
           ptx::tc_fence_after();
@@ -384,7 +329,6 @@ __global__ void __launch_bounds__(512, 1)
             // S/dP of the next sub-tile go into the tensor pipe while the
             // softmax warps turn this one into P^T / dS^T.
             if (u + 1 < nsub) issue_sdp(xx + 1);
-            if (defer_dq && u >= 1) issue_dq(xx - 1);
             const uint32_t st = xx % NSTAGE, sb = xx % C::NDS, pb = xx % C::NPT;
             ptx::mbar_wait_u(&bars[B_P_FULL], xx & 1);
             if (lane == 0) DASH_TRACE_MARK(1, xx);
@@ -404,9 +348,22 @@ __global__ void __launch_bounds__(512, 1)
                                                             dQ_mn + st * Q_STEP, u > 0);
             }
             ptx::mma_commit_e(&bars[B_Q_EMPTY0 + st]);  // Q/dO no longer needed
-            if (!defer_dq) issue_dq(xx);
+            if (xx >= 1) {
+              ptx::mbar_wait_u(&bars[B_DQ_EMPTY], (xx - 1) & 1);
+              ptx::tc_fence_after();
+            }
+            // dQ_local (Alg.1 line 28)
+            if constexpr (D == 128) {
+              umma_gemm_d<128, BR, 128, true, true, 128, 128>(tbase + C::T_DQ, dK_mn,
+                                                              ddS_mn + sb * DS_STEP, false);
+            } else {
+              umma_gemm_d<128, D, 128, true, true, 128, 128>(tbase + C::T_DQ, ddS_mn + sb * DS_STEP,
+                                                             dK_mn, false);
+            }
+            if (lane == 0) DASH_TRACE_MARK(2, xx);
+            ptx::mma_commit_e(&bars[B_DQ_FULL]);
+            ptx::mma_commit_e(&bars[B_DS_EMPTY0 + sb]);
           }
-          if (defer_dq) issue_dq(base + nsub - 1);
           x = base + nsub;
           ptx::mma_commit_e(&bars[B_KV_EMPTY]);
           ptx::mma_commit_e(&bars[B_ACC_FULL]);
@@ -417,32 +374,18 @@ __global__ void __launch_bounds__(512, 1)
     }
   } else if (warp == 2 || warp == 3) {
     // ======================== ordered dQ reducers ==========================
-    // (PAIR: CTA 0 reduces for the pair and claims jobs for both CTAs; the
-    // reducer warps of CTA 1 only follow the job slots.)
     {  // whole warp converged; one elected lane owns the bulk groups
       const uint32_t rid = static_cast<uint32_t>(warp - 2);
       const bool det = args.deterministic != 0;
-      const bool reduces = !PAIR || crank == 0;
       uint32_t it_job = 0, x = 0;
-      // Claim job number it for this CTA (and its peer): slot it & 1.
-      auto claim = [&](uint32_t it) {
-        const int g = atomicAdd(args.job_counter, 1);
-        job_slot[it & 1] = g;
-        if constexpr (PAIR) {
-          ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(&job_slot[it & 1]), peer), static_cast<uint32_t>(g));
-          ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(&bars[B_JOB0 + (it & 1)]), peer));
-        }
-        ptx::mbar_arrive(&bars[B_JOB0 + (it & 1)]);
-      };
-      if (reduces && rid == 0 && lane == 0) claim(0);
+      if (rid == 0 && lane == 0) {
+        job_slot[0] = atomicAdd(args.job_counter, 1);
+        ptx::mbar_arrive(&bars[B_JOB0]);
+      }
       while (true) {
-        ptx::mbar_wait_cluster(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
+        ptx::mbar_wait(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
         const int g = job_slot[it_job & 1];
         if (g >= args.total_jobs) break;
-        if (!reduces) {
-          ++it_job;
-          continue;
-        }
         const JobView jv = decode_job(args, g);
         for (int t = jv.t0; t < jv.t1; ++t) {
           const int2 tk = args.tasks[t];
@@ -450,7 +393,7 @@ __global__ void __launch_bounds__(512, 1)
           for (int sub = 0; sub < NSUB; ++sub) {
            for (int h = 0; h < C::NUNIT; ++h, ++x) {  // x counts staging units here
             if ((x & 1) != rid) continue;
-            const int urow = q * QT + sub * BR + h * C::STG_ROWS;  // first Q row of the unit
+            const int urow = q * 128 + sub * BR + h * C::STG_ROWS;  // first Q row of the unit
             int* ticket = args.tickets + static_cast<size_t>(jv.bh) * n_units + urow / C::STG_ROWS;
             if (det) {
               // Wait until the global order grants this block its turn (Alg.1 line 33).
@@ -519,7 +462,10 @@ __global__ void __launch_bounds__(512, 1)
         if (lane == 0) ptx::mbar_arrive(&bars[B_JOB_DONE]);
         if (rid == 0) {
           ptx::mbar_wait(&bars[B_JOB_DONE], it_job & 1);
-          if (lane == 0) claim(it_job + 1);
+          if (lane == 0) {
+            job_slot[(it_job + 1) & 1] = atomicAdd(args.job_counter, 1);
+            ptx::mbar_arrive(&bars[B_JOB0 + ((it_job + 1) & 1)]);
+          }
         }
         __syncwarp();
         ++it_job;
@@ -534,7 +480,7 @@ __global__ void __launch_bounds__(512, 1)
     const int c_base = wg * NC;
     uint32_t it_job = 0, x = 0, acc_cnt = 0;
     while (true) {
-      ptx::mbar_wait_cluster(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
+      ptx::mbar_wait(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
       const int g = job_slot[it_job & 1];
       ++it_job;
       if (g >= args.total_jobs) break;
@@ -542,9 +488,8 @@ __global__ void __launch_bounds__(512, 1)
       for (int t = jv.t0; t < jv.t1; ++t) {
         const int2 tk = args.tasks[t];
         const int kv = tk.x & 0xFFFF, q = tk.x >> 16;
-        const int kv_row = kv * QT + crank * 128 + row;  // this thread's KV row in the sequence
-        for (int sub = 0; sub < NSUB; ++sub) {
-          if (!live(kv, q, sub)) continue;
+        const bool diag = args.causal && (kv == q);
+        for (int sub = 0; sub < NSUB; ++sub, ++x) {
           const uint32_t st = x % NSTAGE, sb = x % C::NDS, pb = x % C::NPT;
           uint8_t* pdS = smem + C::OFF_DS + sb * C::P_BYTES;
           ptx::mbar_wait(&bars[B_S_FULL], x & 1);
@@ -565,8 +510,7 @@ __global__ void __launch_bounds__(512, 1)
               ptx::mbar_arrive(&bars[B_S_EMPTY]);
             }
             uint32_t pk[16], dk2[16];
-            // causal: key row > query row -> P = 0; columns c < mask_from are masked
-            const int mask_from = args.causal ? (kv_row - (q * QT + sub * BR + cc0)) : -1;
+            const int mask_from = diag ? (row - sub * BR - cc0) : -1;  // mask cols c < mask_from
 #pragma unroll
             for (int c4 = 0; c4 < 8; ++c4) {
               const float4 l4 = *reinterpret_cast<const float4*>(Lrow + cc0 + c4 * 4);
@@ -578,7 +522,7 @@ __global__ void __launch_bounds__(512, 1)
               for (int e = 0; e < 4; ++e) {
                 const int c = c4 * 4 + e;
                 float pv = fast_exp2(fmaf(s[c], args.scale_log2, Lv[e]));
-                if (c < mask_from) pv = 0.f;
+                if (c < mask_from) pv = 0.f;  // causal: key row > query row
                 p[e] = pv;
                 ds[e] = pv * (dp[c] - Dv[e]);
               }
@@ -611,7 +555,6 @@ __global__ void __launch_bounds__(512, 1)
           ptx::fence_async_smem();
           ptx::mbar_arrive(&bars[B_P_FULL]);
           if (row == 0 && wg == 0) DASH_TRACE_MARK(4, x);
-          ++x;
         }
         // End of a KV segment: dK/dV epilogue (local reduction done).
         const bool seg_end = (t + 1 == jv.t1) || ((args.tasks[t + 1].x & 0xFFFF) != kv);
@@ -619,7 +562,7 @@ __global__ void __launch_bounds__(512, 1)
           ptx::mbar_wait(&bars[B_ACC_FULL], acc_cnt & 1);
           ++acc_cnt;
           ptx::tc_fence_after();
-          const size_t grow = (static_cast<size_t>(jv.b) * args.N + kv_row) * args.H + jv.h;
+          const size_t grow = (static_cast<size_t>(jv.b) * args.N + kv * 128 + row) * args.H + jv.h;
           __nv_bfloat16* dvp = args.dv + grow * D;
           __nv_bfloat16* dkp = args.dk + grow * D;
 #pragma unroll 1
@@ -650,124 +593,76 @@ __global__ void __launch_bounds__(512, 1)
     }
   } else {
     // ================== dQ drain: TMEM -> fp32 SW128 staging ==================
-    // PAIR, CTA 1: its partial goes into its own staging buffer for CTA 0 to
-    // read (PEER_FULL / PEER_EMPTY).  PAIR, CTA 0: adds CTA 1's partial (same
-    // swizzled offsets, ld.shared::cluster) to its own before staging.
     const int tl = (warp & 3) * 32 + lane;  // TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    uint8_t* stg = smem + C::OFF_DQ;
-    const uint32_t peer_stg = PAIR ? ptx::mapa(ptx::smem_u32(stg), peer) : 0;
-    uint32_t it_job = 0, x = 0, pc = 0;
+    uint32_t it_job = 0, x = 0;
     while (true) {
-      ptx::mbar_wait_cluster(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
+      ptx::mbar_wait(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
       const int g = job_slot[it_job & 1];
       ++it_job;
       if (g >= args.total_jobs) break;
       const JobView jv = decode_job(args, g);
-      for (int t = jv.t0; t < jv.t1; ++t) {
-        const int kv = args.tasks[t].x & 0xFFFF, q = args.tasks[t].x >> 16;
-        for (int sub = 0; sub < NSUB; ++sub) {
-          if (!live(kv, q, sub)) continue;
-          ptx::mbar_wait(&bars[B_DQ_FULL], x & 1);
-          ptx::tc_fence_after();
-          if (tl == 0) DASH_TRACE_MARK(5, x);
-          float v[64];
-          ptx::tmem_ld32(tbase + lane_off + C::T_DQ, *reinterpret_cast<float(*)[32]>(v));
-          ptx::tmem_ld32(tbase + lane_off + C::T_DQ + 32, *reinterpret_cast<float(*)[32]>(v + 32));
-          ptx::tmem_wait_ld();
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(&bars[B_DQ_EMPTY]);
-          const int urow = q * QT + sub * BR;  // first Q row of the sub-tile (STG_ROWS == BR)
-          if (args.dump) {
-            // verification: this CTA's partial -> dump[bh][kv128][row][:] (kv128 = 128-row KV tile)
-            float* dp = args.dump + ((static_cast<size_t>(jv.bh) * (args.N / 128) +
-                                      (kv * QT + crank * 128) / 128) * args.N + urow) * D;
-            if constexpr (D == 128) {
+      const int nx = (jv.t1 - jv.t0) * NSUB;
+      for (int u = 0; u < nx; ++u, ++x) {
+        ptx::mbar_wait(&bars[B_DQ_FULL], x & 1);
+        ptx::tc_fence_after();
+        if (tl == 0) DASH_TRACE_MARK(5, x);
+        float v[64];
+        ptx::tmem_ld32(tbase + lane_off + C::T_DQ, *reinterpret_cast<float(*)[32]>(v));
+        ptx::tmem_ld32(tbase + lane_off + C::T_DQ + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+        ptx::tmem_wait_ld();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&bars[B_DQ_EMPTY]);
+        if (args.dump) {
+          // verification: the partial of (KV tile kv, these Q rows) -> dump[bh][kv][row][:]
+          const int2 tk = args.tasks[jv.t0 + u / NSUB];
+          const int urow0 = (tk.x >> 16) * 128 + (u % NSUB) * BR;
+          float* dp = args.dump + ((static_cast<size_t>(jv.bh) * (args.N / 128) + (tk.x & 0xFFFF)) *
+                                       args.N + urow0) * D;
+          if constexpr (D == 128) {  // lane tl = d index, v[c] = Q row c
 #pragma unroll
-              for (int c = 0; c < BR; ++c) dp[c * D + tl] = v[c];
-            } else {
+            for (int c = 0; c < BR; ++c) dp[c * D + tl] = v[c];
+          } else {  // lane tl = Q row, v[c] = d column c
 #pragma unroll
-              for (int c = 0; c < 64; ++c) dp[tl * D + c] = v[c];
-            }
+            for (int c = 0; c < 64; ++c) dp[tl * D + c] = v[c];
           }
-          // byte offset in the SW128 fp32 staging layout of element e of this thread
-          auto stg_off = [&](int e) -> uint32_t {
-            if constexpr (D == 128) {  // lane tl = d index, v[e] = Q row e
-              const int blk = tl >> 5, chunk = (tl & 31) >> 2, w = tl & 3;
-              return blk * C::STG_ROWS * 128 + e * 128 + ((chunk ^ (e & 7)) << 4) + w * 4;
-            } else {  // lane tl = Q row, v[e] = d column e
-              const int cc = e >> 2, blk = cc >> 3, chunk = cc & 7;
-              return blk * BR * 128 + tl * 128 + ((chunk ^ (tl & 7)) << 4) + (e & 3) * 4;
+        }
+        uint8_t* stg = smem + C::OFF_DQ;
+#pragma unroll
+        for (int h = 0; h < C::NUNIT; ++h) {
+          const uint32_t y = x * C::NUNIT + h;  // staging unit
+          if (args.debug & 4) continue;  // timing experiment: no staging (pure compute pipeline)
+          if (y >= 1) ptx::mbar_wait(&bars[B_STG_EMPTY], (y - 1) & 1);
+          // Stage STG_ROWS rows of the fp32 partial as SW128 boxes of 32 columns.
+          if constexpr (D == 128) {
+            // lane tl = d index, v[c] = Q row c of the sub-tile
+            const int blk = tl >> 5, chunk = (tl & 31) >> 2, w = tl & 3;
+#pragma unroll
+            for (int c = 0; c < C::STG_ROWS; ++c) {
+              const uint32_t off =
+                  blk * C::STG_ROWS * 128 + c * 128 + ((chunk ^ (c & 7)) << 4) + w * 4;
+              *reinterpret_cast<float*>(stg + off) = v[h * C::STG_ROWS + c];
             }
-          };
-          if (PAIR && crank == 1) {
-            // hand the partial to CTA 0 (after it has read the previous one)
-            if (x >= 1) ptx::mbar_wait_cluster(&bars[B_PEER_EMPTY], (x - 1) & 1);
+          } else {
+            // lane tl = Q row, v[c] = d column c
 #pragma unroll
-            for (int e = 0; e < 64; e += 4) {
-              if constexpr (D == 128) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) *reinterpret_cast<float*>(stg + stg_off(e + k)) = v[e + k];
-              } else {
-                *reinterpret_cast<float4*>(stg + stg_off(e)) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
-              }
-            }
-            ptx::bar_sync(1, 128);
-            if (tl == 0) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(&bars[B_PEER_FULL]), peer));
-            if (tl == 0) DASH_TRACE_MARK(6, x);
-            ++x;
-            continue;
-          }
-          if (PAIR && live_r(kv, q, sub, 1)) {
-            // p0 + p1: CTA 1's partial of the same Q rows, fixed order (AMB-26)
-            ptx::mbar_wait_cluster(&bars[B_PEER_FULL], pc & 1);
-#pragma unroll
-            for (int e = 0; e < 64; e += 16) {
-              float r[16];
-              if constexpr (D == 128) {
-#pragma unroll
-                for (int k = 0; k < 16; ++k) r[k] = ptx::ld_cluster_f32(peer_stg + stg_off(e + k));
-              } else {
-#pragma unroll
-                for (int k = 0; k < 16; k += 4) {
-                  const float4 f = ptx::ld_cluster_f32x4(peer_stg + stg_off(e + k));
-                  r[k] = f.x; r[k + 1] = f.y; r[k + 2] = f.z; r[k + 3] = f.w;
-                }
-              }
-#pragma unroll
-              for (int k = 0; k < 16; ++k) v[e + k] += r[k];
-            }
-            ptx::bar_sync(1, 128);  // every thread has its peer values: CTA 1 may reuse its buffer
-            if (tl == 0) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(&bars[B_PEER_EMPTY]), peer));
-            ++pc;
-          }
-          if (args.debug & 4) {  // timing experiment: no staging (pure compute pipeline)
-            ++x;
-            continue;
-          }
-          if (x >= 1) ptx::mbar_wait(&bars[B_STG_EMPTY], (x - 1) & 1);
-          // Stage the fp32 partial as SW128 boxes of 32 columns.
-#pragma unroll
-          for (int e = 0; e < 64; e += 4) {
-            if constexpr (D == 128) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) *reinterpret_cast<float*>(stg + stg_off(e + k)) = v[e + k];
-            } else {
-              *reinterpret_cast<float4*>(stg + stg_off(e)) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+            for (int cc = 0; cc < 16; ++cc) {
+              const int blk = cc >> 3, chunk = cc & 7;
+              const uint32_t off = blk * BR * 128 + tl * 128 + ((chunk ^ (tl & 7)) << 4);
+              *reinterpret_cast<float4*>(stg + off) =
+                  make_float4(v[cc * 4], v[cc * 4 + 1], v[cc * 4 + 2], v[cc * 4 + 3]);
             }
           }
           ptx::fence_async_smem();
-          ptx::mbar_arrive(&bars[B_STG_FULL0 + (x & 1)]);
-          if (tl == 0) DASH_TRACE_MARK(6, x);
-          ++x;
+          ptx::mbar_arrive(&bars[B_STG_FULL0 + (y & 1)]);
         }
+        if (tl == 0) DASH_TRACE_MARK(6, x);
       }
     }
   }
 
   ptx::tc_fence_before();
   __syncthreads();
-  if constexpr (PAIR) ptx::cluster_sync();  // no remote smem access may outlive the peer
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tbase);

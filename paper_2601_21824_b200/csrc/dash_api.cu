@@ -135,7 +135,7 @@ const DevTable* device_table(int dev, const ScheduleTable* t) {
 // Optional in-kernel clock64 trace (dash_attn_bwd_trace), host-thread-local.
 thread_local unsigned long long* g_trace = nullptr;
 thread_local int g_trace_cap = 0;
-// Optional dump of every staged dQ partial (dash_attn_bwd_dump), host-thread-local.
+// Optional dump of every dQ partial (dash_attn_bwd_dump), host-thread-local.
 thread_local float* g_dump = nullptr;
 
 // Optional per-kernel event timing (dash_profile_begin/end).
@@ -166,73 +166,26 @@ void prof_mark(cudaStream_t st) {
   p.ev.push_back(e);
 }
 
-// Largest number of co-resident 2-CTA clusters of the pair kernel (cached per device).
 template <int D>
-int max_pair_clusters(int dev) {
-  static std::mutex mu;
-  static std::map<int, int> cache;
-  std::lock_guard<std::mutex> lock(mu);
-  auto it = cache.find(dev);
-  if (it != cache.end()) return it->second;
-  using C = BwdCfg<D>;
-  auto kern = dash_bwd_kernel<D, true>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * device_sms(dev));
-  cfg.blockDim = dim3(C::NTHREADS);
-  cfg.dynamicSmemBytes = C::SMEM_BYTES;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
-  cache[dev] = n;
-  return n;
-}
-
-// Pair mode (2-CTA clusters, 256-row schedule tiles; AMB-26) whenever the
-// sequence is a multiple of 256 -- except Symmetric Shift with an odd number
-// of 256-row tiles, which runs on 128-row tiles instead (AMB-10).  DASH_PAIR=0
-// forces the single-CTA kernel (comparison / fallback).
-bool use_pair(const dash_shape* s, int causal, int schedule) {
-  static const bool enabled = [] {
-    const char* e = std::getenv("DASH_PAIR");
-    return !(e && e[0] == '0');
-  }();
-  if (!enabled || s->seqlen % 256) return false;
-  if (schedule == kShift && causal && (s->seqlen / 256) % 2) return false;
-  return true;
-}
-
-template <int D, bool PAIR>
 dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const void* v,
                        const void* o, const void* dout, const float* lse, void* dq, void* dk,
                        void* dv, int causal, int schedule, int deterministic, void* workspace,
                        cudaStream_t stream) {
   using C = BwdCfg<D>;
-  constexpr int QT = PAIR ? 256 : 128;
-  const int n = s->seqlen / QT;
+  const int n = s->seqlen / 128;
   const ScheduleTable* tab = cached_schedule(schedule, n, causal ? kCausal : kFull);
   if (!tab) return DASH_ERR_UNSUPPORTED;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return DASH_ERR_CUDA;
   const int sms = device_sms(dev);
   const int total_jobs = tab->jobs * s->batch * s->heads;
-  // resident job slots: CTAs (single) or 2-CTA clusters (pair)
-  const int slots = PAIR ? max_pair_clusters<D>(dev) : sms;
-  if (slots < 1) return DASH_ERR_UNSUPPORTED;
-  const int resident = total_jobs < slots ? total_jobs : slots;
+  int grid = total_jobs < sms ? total_jobs : sms;
   static const int debug_bits = [] {
     const char* e = std::getenv("DASH_DEBUG");
     return e ? std::atoi(e) : 0;
   }();
 
-  // SHIFT needs every job of a head co-resident (AMB-12).
-  if (schedule == kShift && tab->jobs > resident) return DASH_ERR_UNSUPPORTED;
+  if (schedule == kShift && tab->jobs > grid) return DASH_ERR_UNSUPPORTED;
   const DevTable* dt = device_table(dev, tab);
   if (!dt) return DASH_ERR_CUDA;
 
@@ -294,28 +247,20 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     a.trace_cap = g_trace_cap;
     a.debug = debug_bits;
     a.dump = g_dump;
-    auto kern = dash_bwd_kernel<D, PAIR>;
+    auto kern = dash_bwd_kernel<D>;
     static bool attr_set = false;
     if (!attr_set) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
       attr_set = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(PAIR ? 2 * resident : resident);
+    cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(C::NTHREADS);
     cfg.dynamicSmemBytes = C::SMEM_BYTES;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
-    if (PAIR) {
-      // co-residency: the grid never exceeds cudaOccupancyMaxActiveClusters
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = 2;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-    } else {
-      attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for SHIFT (AMB-12)
-      attr[0].val.cooperative = 1;
-    }
+    attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for SHIFT (AMB-12)
+    attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tdo, tacc, a) != cudaSuccess)
@@ -439,16 +384,11 @@ DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const voi
   if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_SHIFT) return DASH_ERR_INVALID_ARG;
   if (workspace_bytes < ws_layout(s).total) return DASH_ERR_WORKSPACE;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool pair = use_pair(s, causal, schedule);
   if (s->head_dim == 128)
-    return pair ? launch_bwd<128, true>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule,
-                                        deterministic, workspace, st)
-                : launch_bwd<128, false>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule,
-                                         deterministic, workspace, st);
-  return pair ? launch_bwd<64, true>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule,
-                                     deterministic, workspace, st)
-              : launch_bwd<64, false>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule,
-                                      deterministic, workspace, st);
+    return launch_bwd<128>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule, deterministic,
+                           workspace, st);
+  return launch_bwd<64>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule, deterministic,
+                        workspace, st);
 }
 
 DASH_API dash_status dash_attn_bwd_trace(const dash_shape* s, const void* q, const void* k,
@@ -465,11 +405,6 @@ DASH_API dash_status dash_attn_bwd_trace(const dash_shape* s, const void* q, con
   g_trace = nullptr;
   g_trace_cap = 0;
   return r;
-}
-
-DASH_API int dash_attn_bwd_tile_rows(const dash_shape* s, int causal, int schedule) {
-  if (!shape_ok(s)) return 0;
-  return use_pair(s, causal, schedule) ? 256 : 128;
 }
 
 DASH_API size_t dash_attn_bwd_dump_bytes(const dash_shape* s) {

@@ -96,92 +96,8 @@ __device__ __forceinline__ void mbar_wait_u(uint64_t* bar, uint32_t parity) {
       "r"(parity), "l"(&g_dash_abort)
       : "memory");
 }
-// Same, acquiring at cluster scope (job slots written by the peer CTA of a pair).
-__device__ __forceinline__ void mbar_wait_u_cl(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t.reg .b32 ab;\n\t"
-      "DASH_WAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DASH_DONEC_%=;\n\t"
-      "ld.volatile.global.u32 ab, [%2];\n\t"
-      "setp.ne.u32 P1, ab, 0;\n\t"
-      "@P1 bra DASH_DONEC_%=;\n\t"
-      "bra DASH_WAITC_%=;\n\t"
-      "DASH_DONEC_%=:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity), "l"(&g_dash_abort)
-      : "memory");
-}
 __device__ __forceinline__ bool aborted() {
   return *reinterpret_cast<volatile int*>(&g_dash_abort) != 0;
-}
-
-// ---- clusters (CTA pairs) ---------------------------------------------------------
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-// Shared-memory address of the same variable in CTA `rank` of the cluster.
-__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-  return r;
-}
-// Arrive (release, cluster scope) on an mbarrier of another CTA of the cluster.
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred P;\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, P;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-// Wait (acquire, cluster scope) for data a peer CTA released with mbar_arrive_remote.
-__device__ __noinline__ void mbar_wait_cluster_slow(uint64_t* bar, uint32_t parity) {
-  const long long t0 = clock64();
-  while (!mbar_try_wait_cluster(bar, parity)) {
-    if (*reinterpret_cast<volatile int*>(&g_dash_abort)) return;
-    if (clock64() - t0 > kWatchdogCycles) {
-      printf("dash watchdog: block %d thread %d stuck on cluster mbarrier smem+0x%x parity %u\n",
-             blockIdx.x, threadIdx.x, smem_u32(bar), parity);
-      atomicExch(&g_dash_abort, 1);
-      return;
-    }
-  }
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  if (mbar_try_wait_cluster(bar, parity)) return;
-  mbar_wait_cluster_slow(bar, parity);
-}
-__device__ __forceinline__ float ld_cluster_f32(uint32_t cluster_addr) {
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr) : "memory");
-  return v;
-}
-__device__ __forceinline__ float4 ld_cluster_f32x4(uint32_t cluster_addr) {
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(cluster_addr)
-               : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, uint32_t v) {
-  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
-}
-__device__ __forceinline__ void fence_acq_rel_cluster() {
-  asm volatile("fence.acq_rel.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
 }
 
 // ---- proxy fences -----------------------------------------------------------

@@ -57,8 +57,6 @@ def _load():
     lib.dash_attn_bwd_trace.restype = st
     lib.dash_attn_bwd_trace.argtypes = [SP, vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp, sz,
                                         vp, i, vp]
-    lib.dash_attn_bwd_tile_rows.restype = i
-    lib.dash_attn_bwd_tile_rows.argtypes = [SP, i, i]
     lib.dash_attn_bwd_dump_bytes.restype = sz
     lib.dash_attn_bwd_dump_bytes.argtypes = [SP]
     lib.dash_attn_bwd_dump.restype = st
@@ -181,13 +179,6 @@ def attn_bwd_trace(q, k, v, o, dout, lse, causal: bool, schedule, deterministic,
                                     workspace.numel(), _ptr(trace), trace_cap, _stream(q)),
            "dash_attn_bwd_trace")
     return (dq, dk, dv), trace
-
-
-def tile_rows(shape_bnhd, causal: bool, schedule) -> int:
-    """dash_attn_bwd_tile_rows: 256 (2-CTA pair tiles) or 128."""
-    B, N, H, d = shape_bnhd
-    shp = Shape(B, N, H, d, 0.0)
-    return int(_lib.dash_attn_bwd_tile_rows(ctypes.byref(shp), int(causal), _sched(schedule)))
 
 
 def attn_bwd_dump(q, k, v, o, dout, lse, causal: bool, schedule, deterministic=True, scale=None,

@@ -7,4 +7,5 @@ for pr in 1 0; do
   DASH_PAIR=$pr timeout 300 python scripts/exp_reduce_path.py 512,2048,16384 128 causal
   DASH_PAIR=$pr timeout 300 python scripts/exp_reduce_path.py 512,2048,16384 128 full
   DASH_PAIR=$pr timeout 300 python scripts/exp_reduce_path.py 2048,16384 64 causal
-done 2>&1 | grep -E "DEBUG|PAIR" | tee gpurun_out/exp_v9.txt
+done 2>&1 | grep -E "DEBUG|PAIR" | tee gpurun_out/exp_v9b.txt
+timeout 120 python scripts/grid_probe.py 2>&1 | tail -3
