@@ -279,7 +279,7 @@ def workload_config(args, world):
             f"-{TOKENS}tok-hidden{HIDDEN}")
     return {"workload": name, "seqlens": list(SEQLENS), "total_tokens": TOKENS,
             "hidden": HIDDEN, "head_dim": args.head_dim, "mask": "causal" if causal else "full",
-            "schedule": args.schedule, "per_gpu_heads_x_batch": [list(s[::2]) for s in shapes(args.head_dim)],
+            "schedule": args.schedule, "acc_split": args.acc_split, "per_gpu_heads_x_batch": [list(s[::2]) for s in shapes(args.head_dim)],
             "parallelism": f"bh-shard x{world}", "l2": "inputs > L2 (5 x 64 MiB per sweep point, 126 MB L2)"}
 
 
@@ -292,6 +292,8 @@ def main():
     ap.add_argument("--head-dim", type=int, default=128)
     ap.add_argument("--full", action="store_true", help="full mask instead of causal")
     ap.add_argument("--schedule", default=None)
+    ap.add_argument("--acc-split", type=int, default=None,
+                    help="interleaved dQ accumulators W in {1,2,4} (AMB-27); default: the library's automatic choice")
     ap.add_argument("--no-sweep", action="store_true", help="skip the per-schedule sweep table")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--no-e2e", action="store_true")
@@ -308,6 +310,9 @@ def main():
     import torch
     world, rank, local = dist_setup(args)
     from paper_2601_21824_b200 import dash
+    if args.acc_split is not None:
+        dash.set_acc_split(args.acc_split)
+    args.acc_split = dash.acc_split()  # 0 = automatic (per seqlen: sweep rows)
     d = args.head_dim
     seqlens = tuple(int(x) for x in args.seqlens.split(",")) if args.seqlens else SEQLENS
     probs = [(s, make_problem(*s, causal, rank, dash, torch)) for s in shapes(d, seqlens)]
@@ -382,14 +387,22 @@ def main():
         del host
 
     # --- per-schedule sweep table (N = 1 only) ----------------------------------------
+    # Every schedule at the bench's accumulator split W (AMB-27) and at W = 1,
+    # the paper's single ordered accumulator per dQ tile, plus the atomic variant.
     sweep = None
     if world == 1 and not args.no_sweep:
         sweep = []
+        w_bench = dash.acc_split()
         for s, g in probs:
-            row = {"seqlen": s[1], "batch": s[0], "heads": s[2]}
+            row = {"seqlen": s[1], "batch": s[0], "heads": s[2], "acc_split": dash.acc_split(s[1])}
             f = fa_flops(*s, causal)
-            for name, sched, det in (("naive", "naive", True), ("descending", "descending", True),
-                                     ("shift", "shift", True), ("atomic", "naive", False)):
+            cases = [("naive", "naive", True, w_bench), ("descending", "descending", True, w_bench),
+                     ("shift", "shift", True, w_bench), ("atomic", "naive", False, w_bench)]
+            if dash.acc_split(s[1]) != 1:
+                cases += [("naive_w1", "naive", True, 1), ("descending_w1", "descending", True, 1),
+                          ("shift_w1", "shift", True, 1)]
+            for name, sched, det, w in cases:
+                dash.set_acc_split(w)
                 try:
                     t = time_steps(torch, lambda: run_bwd(dash, g, causal, sched, det),
                                    max(3, args.steps), 2, 1)
@@ -397,15 +410,20 @@ def main():
                 except dash.DashError as e:
                     row[name] = None
                     row[name + "_error"] = str(e)
-            best = max(v for v in (row.get("descending"), row.get("shift")) if v is not None)
-            gap = row["atomic"] - row["naive"]
-            row["best_dash"] = best
-            if abs(gap) < 0.02 * row["atomic"]:
-                row["gap_closed"] = None
-                row["pass"] = best >= 0.98 * row["naive"]
-            else:
-                row["gap_closed"] = (best - row["naive"]) / gap
-                row["pass"] = row["gap_closed"] >= 0.5
+            dash.set_acc_split(w_bench)
+            for suffix in ("", "_w1"):
+                if row.get("naive" + suffix) is None:
+                    continue
+                best = max(v for v in (row.get("descending" + suffix), row.get("shift" + suffix))
+                           if v is not None)
+                gap = row["atomic"] - row["naive" + suffix]
+                row["best_dash" + suffix] = best
+                if abs(gap) < 0.02 * row["atomic"]:
+                    row["gap_closed" + suffix] = None
+                    row["pass" + suffix] = best >= 0.98 * row["naive" + suffix]
+                else:
+                    row["gap_closed" + suffix] = (best - row["naive" + suffix]) / gap
+                    row["pass" + suffix] = row["gap_closed" + suffix] >= 0.5
             sweep.append(row)
 
     cpu = None

@@ -187,6 +187,23 @@ dash_status dash_attn_bwd_trace(const dash_shape* shape, const void* q, const vo
                                 int deterministic, void* workspace, size_t workspace_bytes,
                                 unsigned long long* trace, int trace_cap, void* stream);
 
+/* Number W of interleaved fp32 dQ accumulators the deterministic backward
+ * uses (AMB-27).  W = 1 is the paper's single global order per dQ tile
+ * (P:395-397).  W = 2 or 4: the contribution of rank k is added, in rank
+ * order, into accumulator k mod W under that accumulator's own ticket, and
+ * the convert kernel sums the accumulators in index order -- a fixed order,
+ * so results stay bitwise deterministic, while consecutive adds into one
+ * accumulator are W schedule steps apart instead of one.
+ * dash_attn_bwd_acc_split(seqlen) returns the W a call with that N uses
+ * (seqlen not a positive multiple of 128: returns the setting itself, 0 =
+ * automatic).  The setting defaults to automatic (W = 4 for N >= 8192, else
+ * 2; depends on N only), or to the DASH_ACC_SPLIT environment variable.
+ * dash_attn_bwd_set_acc_split(w), w in {0 (automatic), 1, 2, 4}, changes it
+ * for later calls (host-global, not for concurrent use; other values:
+ * DASH_ERR_INVALID_ARG).  The atomic variant always uses one accumulator. */
+int dash_attn_bwd_acc_split(int seqlen);
+dash_status dash_attn_bwd_set_acc_split(int w);
+
 /* Verification variant of dash_attn_bwd (same arguments and results) that
  * also writes every dQ partial dQ_local = dS K_i (Alg.1 line 28; fp32,
  * unscaled) as it is handed to the ordered reduction: partials is device

@@ -56,6 +56,12 @@ struct BwdArgs {
   int debug;  // timing experiments only (env DASH_DEBUG): bit 0 skips the dQ reduce ops,
              // bit 2 skips the dQ staging (with bit 0: the compute pipeline alone)
   float* dump;  // verification only: every dQ partial, [B*H][N/128][N][d] fp32
+  // Interleaved accumulation (AMB-27): split = W in {1, 2, 4}.  The contribution
+  // of rank k goes into accumulator k % W (dQacc + (k % W) * B*H*N*d) in the
+  // order of its ticket set k % W (value k / W); the convert kernel adds the W
+  // accumulators in index order.  W = 1 is the paper's single global order.
+  int split;
+  int n_tickets;  // tickets per accumulator
 };
 
 // Per-(CTA, sub-tile) clock64 stamps for pipeline analysis; a null trace
@@ -67,13 +73,22 @@ struct BwdArgs {
           clock64();                                                                      \
   } while (0)
 
-template <int D>
+// V selects the smem split between the Q/dO ring and the dQ staging:
+// V = 0: NSTAGE-deep ring (3 at d = 128), one staging buffer of a whole
+//        sub-tile's partial (one ticket per sub-tile);
+// V = 1: one staging buffer per reducer (the drain can stage the next partial
+//        while the previous one still waits for its ticket), ring of 2;
+// V = 2: the partial staged and reduced in two halves of BR/2 rows, each with
+//        its own ticket (two shorter hand-offs per sub-tile), one half-size
+//        buffer per reducer, same ring as V = 0.
+template <int D, int V = 0>
 struct BwdCfg {
   static constexpr int NTHREADS = 512;
   static constexpr int BC = 128;                    // KV tile rows (TMEM lanes)
   static constexpr int BR = (D == 128) ? 64 : 128;  // Q sub-tile rows
   static constexpr int NSUB = 128 / BR;             // sub-tiles per schedule Q tile
-  static constexpr int NSTAGE = (D == 128) ? 3 : 2; // Q/dO/L/D ring depth
+  static constexpr int NSTAGE = (D == 128 && V != 1) ? 3 : 2;  // Q/dO/L/D ring depth
+  static constexpr int NSTG = V ? 2 : 1;                       // dQ staging buffers
   static constexpr int NSMX = 2;                    // softmax warpgroups (column halves)
   static constexpr int SMX_COLS = BR / NSMX;        // columns per softmax thread
   static constexpr uint32_t KV_BYTES = BC * D * 2;
@@ -83,7 +98,7 @@ struct BwdCfg {
   // STG_ROWS rows, each with its own ticket.  (Measured: splitting the d = 128
   // partial into 32-row halves to afford a 4-stage Q/dO ring with one dS^T
   // buffer was slower -- the softmax then waits on the dQ MMA.)
-  static constexpr int STG_ROWS = BR;
+  static constexpr int STG_ROWS = V == 2 ? BR / 2 : BR;
   static constexpr int NUNIT = BR / STG_ROWS;  // staging units per sub-tile
   static constexpr uint32_t DQ_BYTES = STG_ROWS * D * 4;
   static constexpr uint32_t OFF_K = 0;
@@ -97,7 +112,7 @@ struct BwdCfg {
   static constexpr bool DS_IN_TMEM = (D == 128);
   static constexpr uint32_t OFF_DS = OFF_DO + NSTAGE * Q_BYTES;  // NDS x dS^T bf16 SW128
   static constexpr uint32_t OFF_DQ = OFF_DS + NDS * P_BYTES;     // fp32 SW128 staging buffer
-  static constexpr uint32_t OFF_L = OFF_DQ + DQ_BYTES;           // NSTAGE x BR floats
+  static constexpr uint32_t OFF_L = OFF_DQ + NSTG * DQ_BYTES;    // NSTAGE x BR floats
   static constexpr uint32_t OFF_DV = OFF_L + NSTAGE * BR * 4;    // NSTAGE x BR floats
   static constexpr uint32_t OFF_BAR = OFF_DV + NSTAGE * BR * 4;
   static constexpr int NBAR = 32;
@@ -129,9 +144,10 @@ enum : int {
   B_DQ_FULL = 7, B_DQ_EMPTY = 8,       // dQ partial in TMEM (commit) / drained (128)
   B_PT_EMPTY0 = 9,                     // P^T TMEM buffer consumed by dV (commit)
   B_DST_EMPTY = 10,                    // dS^T TMEM buffer consumed by dK (commit)
+  B_STG_EMPTY1 = 11,                   // staging buffer 1 read by the reduce (1), NSTG = 2
   B_DS_EMPTY0 = 22, B_DS_EMPTY1 = 23,  // dS^T smem buffer consumed by dK, dQ (commit)
   B_ACC_FULL = 12, B_ACC_EMPTY = 13,   // dK/dV complete (commit) / drained (256)
-  B_STG_EMPTY = 14,                    // staging read by the reduce (1)
+  B_STG_EMPTY = 14,                    // staging (buffer 0) read by the reduce (1)
   B_JOB_DONE = 15,                     // both reducers released the job (2)
   B_STG_FULL0 = 16, B_STG_FULL1 = 17,  // staging written, for reducer x & 1 (128)
   B_Q_FULL0 = 18,                      // + stage (<= 4): Q/dO/L/D loaded (tx)
@@ -179,18 +195,19 @@ __device__ __forceinline__ JobView decode_job(const BwdArgs& a, int g) {
   return j;
 }
 
-template <int D>
+template <int D, int V>
 __global__ void __launch_bounds__(512, 1)
     dash_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_dqacc, const BwdArgs args) {
-  using C = BwdCfg<D>;
-  constexpr int BR = C::BR, NSUB = C::NSUB, NSTAGE = C::NSTAGE;
+  using C = BwdCfg<D, V>;
+  constexpr int BR = C::BR, NSUB = C::NSUB, NSTAGE = C::NSTAGE, NSTG = C::NSTG;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t pad = (1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023;
   if (pad > C::SLACK) __trap();
   uint8_t* smem = smem_raw + pad;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  auto stg_empty = [&](uint32_t unit) { return &bars[(unit % NSTG) ? B_STG_EMPTY1 : B_STG_EMPTY]; };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_MISC);
   int* job_slot = reinterpret_cast<int*>(smem + C::OFF_MISC + 8);  // [2]
   float* sL = reinterpret_cast<float*>(smem + C::OFF_L);
@@ -394,14 +411,16 @@ __global__ void __launch_bounds__(512, 1)
            for (int h = 0; h < C::NUNIT; ++h, ++x) {  // x counts staging units here
             if ((x & 1) != rid) continue;
             const int urow = q * 128 + sub * BR + h * C::STG_ROWS;  // first Q row of the unit
-            int* ticket = args.tickets + static_cast<size_t>(jv.bh) * n_units + urow / C::STG_ROWS;
+            const int par = rank % args.split, rank_w = rank / args.split;  // AMB-27
+            int* ticket = args.tickets + static_cast<size_t>(par) * args.n_tickets +
+                          static_cast<size_t>(jv.bh) * n_units + urow / C::STG_ROWS;
             if (det) {
               // Wait until the global order grants this block its turn (Alg.1 line 33).
               // Spin with relaxed loads (an acquire per poll would invalidate L1
               // every iteration); one acquire once the turn has come.
-              if (ptx::ld_acquire(ticket) != rank) {
+              if (ptx::ld_acquire(ticket) != rank_w) {
                 const long long t_start = clock64();
-                while (ptx::ld_relaxed(ticket) != rank) {
+                while (ptx::ld_relaxed(ticket) != rank_w) {
                   __nanosleep(32);
                   if (clock64() - t_start > 8 * ptx::kWatchdogCycles ||
                       *reinterpret_cast<volatile int*>(&ptx::g_dash_abort)) {  // ~35 s bound
@@ -423,13 +442,14 @@ __global__ void __launch_bounds__(512, 1)
             if (!(args.debug & 4)) ptx::mbar_wait(&bars[B_STG_FULL0 + rid], (x >> 1) & 1);
             __syncwarp();
             // Add dQ_local to dQ (Alg.1 line 34); rank 0 stores (no zero-fill needed).
-            const int grow = jv.bh * args.N + urow;  // row of dQacc [B*H*N, D]
-            const uint8_t* stg = smem + C::OFF_DQ;
+            // row of dQacc [W][B*H*N, D]
+            const int grow = (par * args.B * args.H + jv.bh) * args.N + urow;
+            const uint8_t* stg = smem + C::OFF_DQ + (x % NSTG) * C::DQ_BYTES;
             if (lane == 0) {
 #pragma unroll
               for (int blk = 0; blk < D / 32; ++blk) {
                 if (args.debug & 1) break;  // timing experiment: no reduce traffic
-                if (det && rank == 0) {
+                if (det && rank_w == 0) {
                   tma_store_2d(&tm_dqacc, stg + blk * C::STG_ROWS * 128, blk * 32, grow);
                 } else {
                   tma_reduce_add_2d(&tm_dqacc, stg + blk * C::STG_ROWS * 128, blk * 32, grow);
@@ -438,7 +458,7 @@ __global__ void __launch_bounds__(512, 1)
               ptx::bulk_commit();
               if (h == 0) DASH_TRACE_MARK(8, x / C::NUNIT);
               ptx::bulk_wait_read_all();  // staging may be overwritten from here on
-              ptx::mbar_arrive(&bars[B_STG_EMPTY]);
+              ptx::mbar_arrive(stg_empty(x));
               if (h == 0) DASH_TRACE_MARK(11, x / C::NUNIT);
               ptx::bulk_wait_all();
               if (h == 0) DASH_TRACE_MARK(12, x / C::NUNIT);
@@ -449,7 +469,7 @@ __global__ void __launch_bounds__(512, 1)
                 // the bulk group alone does not order the reduce's writes
                 // before the flag (tests/test_gpu_bwd.py catches it).
                 ptx::fence_async_global();
-                ptx::st_release(ticket, rank + 1);
+                ptx::st_release(ticket, rank_w + 1);
               }
               if (h == C::NUNIT - 1) DASH_TRACE_MARK(9, x / C::NUNIT);
             }
@@ -627,12 +647,13 @@ __global__ void __launch_bounds__(512, 1)
             for (int c = 0; c < 64; ++c) dp[tl * D + c] = v[c];
           }
         }
-        uint8_t* stg = smem + C::OFF_DQ;
+        uint8_t* stg0 = smem + C::OFF_DQ;
 #pragma unroll
         for (int h = 0; h < C::NUNIT; ++h) {
           const uint32_t y = x * C::NUNIT + h;  // staging unit
           if (args.debug & 4) continue;  // timing experiment: no staging (pure compute pipeline)
-          if (y >= 1) ptx::mbar_wait(&bars[B_STG_EMPTY], (y - 1) & 1);
+          if (y >= NSTG) ptx::mbar_wait(stg_empty(y), ((y / NSTG) - 1) & 1);
+          uint8_t* stg = stg0 + (y % NSTG) * C::DQ_BYTES;
           // Stage STG_ROWS rows of the fp32 partial as SW128 boxes of 32 columns.
           if constexpr (D == 128) {
             // lane tl = d index, v[c] = Q row c of the sub-tile
@@ -644,13 +665,16 @@ __global__ void __launch_bounds__(512, 1)
               *reinterpret_cast<float*>(stg + off) = v[h * C::STG_ROWS + c];
             }
           } else {
-            // lane tl = Q row, v[c] = d column c
+            // lane tl = Q row, v[c] = d column c; unit h holds rows [h*STG_ROWS, +STG_ROWS)
+            const int r = tl - h * C::STG_ROWS;
+            if (r >= 0 && r < C::STG_ROWS) {
 #pragma unroll
-            for (int cc = 0; cc < 16; ++cc) {
-              const int blk = cc >> 3, chunk = cc & 7;
-              const uint32_t off = blk * BR * 128 + tl * 128 + ((chunk ^ (tl & 7)) << 4);
-              *reinterpret_cast<float4*>(stg + off) =
-                  make_float4(v[cc * 4], v[cc * 4 + 1], v[cc * 4 + 2], v[cc * 4 + 3]);
+              for (int cc = 0; cc < 16; ++cc) {
+                const int blk = cc >> 3, chunk = cc & 7;
+                const uint32_t off = blk * C::STG_ROWS * 128 + r * 128 + ((chunk ^ (r & 7)) << 4);
+                *reinterpret_cast<float4*>(stg + off) =
+                    make_float4(v[cc * 4], v[cc * 4 + 1], v[cc * 4 + 2], v[cc * 4 + 3]);
+              }
             }
           }
           ptx::fence_async_smem();
@@ -721,12 +745,16 @@ __global__ void dash_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
   for (size_t i = gtid; i < n_zero_f4; i += nthreads) zero_f32[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
-// K4: dQ = bf16(scale * dQacc), [B,H,N,d] fp32 -> [B,N,H,d] bf16.
+// K4: dQ = bf16(scale * dQacc), [B,H,N,d] fp32 -> [B,N,H,d] bf16.  With W
+// interleaved accumulators (AMB-27) the sum is ((acc_0 + acc_1) + acc_2) + ...
+// (fp32, in index order) over the min(W, cnt) accumulators a 128-row Q tile
+// with cnt contributions has written (causal: tile j has j + 1).
 template <int D>
 __global__ void dash_dq_convert_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq,
-                                       int B, int N, int H, float scale) {
+                                       int B, int N, int H, float scale, int split, int causal) {
   constexpr int T = D / 8;
   const size_t total = static_cast<size_t>(B) * H * N * T;
+  const size_t plane = static_cast<size_t>(B) * H * N * D;
   for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const int part = static_cast<int>(i % T);
@@ -735,8 +763,16 @@ __global__ void dash_dq_convert_kernel(const float* __restrict__ acc, __nv_bfloa
     const size_t bh = r / N;
     const int h = static_cast<int>(bh % H);
     const int b = static_cast<int>(bh / H);
-    const float4 x0 = *reinterpret_cast<const float4*>(acc + r * D + part * 8);
-    const float4 x1 = *reinterpret_cast<const float4*>(acc + r * D + part * 8 + 4);
+    float4 x0 = *reinterpret_cast<const float4*>(acc + r * D + part * 8);
+    float4 x1 = *reinterpret_cast<const float4*>(acc + r * D + part * 8 + 4);
+    const int cnt = causal ? n / 128 + 1 : N / 128;
+    const int planes = split < cnt ? split : cnt;  // accumulator w holds ranks w, w + W, ...
+    for (int w = 1; w < planes; ++w) {
+      const float4 y0 = *reinterpret_cast<const float4*>(acc + w * plane + r * D + part * 8);
+      const float4 y1 = *reinterpret_cast<const float4*>(acc + w * plane + r * D + part * 8 + 4);
+      x0 = make_float4(x0.x + y0.x, x0.y + y0.y, x0.z + y0.z, x0.w + y0.w);
+      x1 = make_float4(x1.x + y1.x, x1.y + y1.y, x1.z + y1.z, x1.w + y1.w);
+    }
     uint4 out;
     out.x = pack_bf16(x0.x * scale, x0.y * scale);
     out.y = pack_bf16(x0.z * scale, x0.w * scale);

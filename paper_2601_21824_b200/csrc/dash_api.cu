@@ -24,6 +24,24 @@ namespace dash {
 namespace {
 
 constexpr size_t kAlign = 1024;
+constexpr int kDefaultVariant = 0;  // BwdCfg smem variant used unless DASH_VARIANT is set
+// Interleaved dQ accumulators (AMB-27): 0 = automatic (the default), else
+// fixed W in {1, 2, 4}; DASH_ACC_SPLIT overrides the default at load time.
+int g_acc_split = [] {
+  const char* e = std::getenv("DASH_ACC_SPLIT");
+  const int v = e ? std::atoi(e) : 0;
+  return (v == 1 || v == 2 || v == 4) ? v : 0;
+}();
+int acc_split() { return g_acc_split; }
+// W actually used for a problem with n 128-row tiles per head.  Automatic:
+// W = 4 once the per-tile chain is long (n >= 64), else 2 -- measured on
+// B200 (profiles/r01_experiments/acc_split.txt): extra accumulators cost the
+// convert kernel one more fp32 read each, which only pays off at long
+// sequences.  Depends on n only, so (b, h) sharding never changes it.
+int acc_split_for(int n) {
+  if (g_acc_split) return g_acc_split;
+  return n >= 64 ? 4 : 2;
+}
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 bool shape_ok(const dash_shape* s) {
@@ -37,12 +55,16 @@ bool aligned16(const void* p) { return p && (reinterpret_cast<uintptr_t>(p) & 15
 float eff_scale(const dash_shape* s) {
   return s->softmax_scale > 0.f ? s->softmax_scale : 1.0f / std::sqrt(static_cast<float>(s->head_dim));
 }
-int ticket_rows(int d) { return d == 128 ? BwdCfg<128>::STG_ROWS : BwdCfg<64>::STG_ROWS; }
+// ticket granularity for the workspace: the smallest staging unit of any variant
+int ticket_rows(int d) { return d == 128 ? BwdCfg<128, 2>::STG_ROWS : BwdCfg<64, 2>::STG_ROWS; }
 
 struct WsLayout {
   size_t dqacc = 0, dvec = 0, lse2 = 0, tickets = 0, counters = 0, total = 0;
   size_t dqacc_bytes = 0, n_tickets = 0;
 };
+// Up to kMaxSplit interleaved fp32 accumulators (AMB-27), each with its own
+// ticket set: dqacc [W][B,H,N,d], tickets [W][B*H][N / ticket_rows].
+constexpr int kMaxSplit = 4;
 WsLayout ws_layout(const dash_shape* s) {
   WsLayout w;
   const size_t BHN = static_cast<size_t>(s->batch) * s->heads * s->seqlen;
@@ -50,13 +72,13 @@ WsLayout ws_layout(const dash_shape* s) {
   w.n_tickets = static_cast<size_t>(s->batch) * s->heads * (s->seqlen / ticket_rows(s->head_dim));
   size_t off = 0;
   w.dqacc = off;
-  off = align_up(off + w.dqacc_bytes, kAlign);
+  off = align_up(off + kMaxSplit * w.dqacc_bytes, kAlign);
   w.dvec = off;
   off = align_up(off + BHN * 4, kAlign);
   w.lse2 = off;
   off = align_up(off + BHN * 4, kAlign);
   w.tickets = off;
-  off = align_up(off + w.n_tickets * 4, kAlign);
+  off = align_up(off + kMaxSplit * w.n_tickets * 4, kAlign);
   w.counters = off;  // [0] job counter, [1] error flag
   off = align_up(off + 64, kAlign);
   w.total = off;
@@ -166,12 +188,12 @@ void prof_mark(cudaStream_t st) {
   p.ev.push_back(e);
 }
 
-template <int D>
+template <int D, int V>
 dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const void* v,
                        const void* o, const void* dout, const float* lse, void* dq, void* dk,
                        void* dv, int causal, int schedule, int deterministic, void* workspace,
                        cudaStream_t stream) {
-  using C = BwdCfg<D>;
+  using C = BwdCfg<D, V>;
   const int n = s->seqlen / 128;
   const ScheduleTable* tab = cached_schedule(schedule, n, causal ? kCausal : kFull);
   if (!tab) return DASH_ERR_UNSUPPORTED;
@@ -205,7 +227,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
             make_map_2d(&tv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, v, HD, BN, 64, C::BC) &&
             make_map_2d(&tdo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, HD, BN, 64, C::BR) &&
             make_map_2d(&tacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dqacc, D,
-                        BN * static_cast<uint64_t>(s->heads), 32, C::STG_ROWS);
+                        kMaxSplit * BN * static_cast<uint64_t>(s->heads), 32, C::STG_ROWS);
   if (!ok) return DASH_ERR_CUDA;
 
   prof_mark(stream);
@@ -217,7 +239,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     const unsigned gridp = static_cast<unsigned>((threads + block - 1) / block);
     dash_preprocess_kernel<D><<<gridp, block, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse, dvec,
-        lse2, s->batch, s->seqlen, s->heads, tickets, static_cast<int>(w.n_tickets),
+        lse2, s->batch, s->seqlen, s->heads, tickets, static_cast<int>(kMaxSplit * w.n_tickets),
         deterministic ? nullptr : reinterpret_cast<float4*>(dqacc),
         deterministic ? 0 : w.dqacc_bytes / 16, counters);
   }
@@ -246,8 +268,10 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     a.trace = g_trace;
     a.trace_cap = g_trace_cap;
     a.debug = debug_bits;
+    a.split = deterministic ? acc_split_for(n) : 1;
+    a.n_tickets = static_cast<int>(w.n_tickets);
     a.dump = g_dump;
-    auto kern = dash_bwd_kernel<D>;
+    auto kern = dash_bwd_kernel<D, V>;
     static bool attr_set = false;
     if (!attr_set) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
@@ -274,7 +298,8 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     size_t g = (total + block - 1) / block;
     if (g > static_cast<size_t>(sms) * 16) g = static_cast<size_t>(sms) * 16;
     dash_dq_convert_kernel<D><<<static_cast<unsigned>(g), block, 0, stream>>>(
-        dqacc, static_cast<__nv_bfloat16*>(dq), s->batch, s->seqlen, s->heads, eff_scale(s));
+        dqacc, static_cast<__nv_bfloat16*>(dq), s->batch, s->seqlen, s->heads, eff_scale(s),
+        deterministic ? acc_split_for(s->seqlen / 128) : 1, causal ? 1 : 0);
   }
   prof_mark(stream);
   return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ERR_CUDA;
@@ -384,11 +409,19 @@ DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const voi
   if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_SHIFT) return DASH_ERR_INVALID_ARG;
   if (workspace_bytes < ws_layout(s).total) return DASH_ERR_WORKSPACE;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // smem variant (BwdCfg): DASH_VARIANT overrides the default (experiments)
+  static const int variant = [] {
+    const char* e = std::getenv("DASH_VARIANT");
+    return e ? std::atoi(e) : -1;
+  }();
+  const int var = variant >= 0 ? variant : kDefaultVariant;
+#define DASH_LAUNCH(DD, VV)                                                                   \
+  launch_bwd<DD, VV>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule, deterministic, \
+                     workspace, st)
   if (s->head_dim == 128)
-    return launch_bwd<128>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule, deterministic,
-                           workspace, st);
-  return launch_bwd<64>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule, deterministic,
-                        workspace, st);
+    return var == 2 ? DASH_LAUNCH(128, 2) : var == 1 ? DASH_LAUNCH(128, 1) : DASH_LAUNCH(128, 0);
+  return var == 2 ? DASH_LAUNCH(64, 2) : var == 1 ? DASH_LAUNCH(64, 1) : DASH_LAUNCH(64, 0);
+#undef DASH_LAUNCH
 }
 
 DASH_API dash_status dash_attn_bwd_trace(const dash_shape* s, const void* q, const void* k,
@@ -405,6 +438,17 @@ DASH_API dash_status dash_attn_bwd_trace(const dash_shape* s, const void* q, con
   g_trace = nullptr;
   g_trace_cap = 0;
   return r;
+}
+
+DASH_API int dash_attn_bwd_acc_split(int seqlen) {
+  if (seqlen < 128 || seqlen % 128) return acc_split();
+  return acc_split_for(seqlen / 128);
+}
+
+DASH_API dash_status dash_attn_bwd_set_acc_split(int w) {
+  if (w != 0 && w != 1 && w != 2 && w != 4) return DASH_ERR_INVALID_ARG;
+  g_acc_split = w;
+  return DASH_OK;
 }
 
 DASH_API size_t dash_attn_bwd_dump_bytes(const dash_shape* s) {

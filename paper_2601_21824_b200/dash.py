@@ -57,6 +57,10 @@ def _load():
     lib.dash_attn_bwd_trace.restype = st
     lib.dash_attn_bwd_trace.argtypes = [SP, vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp, sz,
                                         vp, i, vp]
+    lib.dash_attn_bwd_acc_split.restype = i
+    lib.dash_attn_bwd_acc_split.argtypes = [i]
+    lib.dash_attn_bwd_set_acc_split.restype = st
+    lib.dash_attn_bwd_set_acc_split.argtypes = [i]
     lib.dash_attn_bwd_dump_bytes.restype = sz
     lib.dash_attn_bwd_dump_bytes.argtypes = [SP]
     lib.dash_attn_bwd_dump.restype = st
@@ -179,6 +183,17 @@ def attn_bwd_trace(q, k, v, o, dout, lse, causal: bool, schedule, deterministic,
                                     workspace.numel(), _ptr(trace), trace_cap, _stream(q)),
            "dash_attn_bwd_trace")
     return (dq, dk, dv), trace
+
+
+def acc_split(seqlen: int = 0) -> int:
+    """dash_attn_bwd_acc_split: the W a call with this seqlen uses (AMB-27);
+    seqlen = 0 returns the setting (0 = automatic)."""
+    return int(_lib.dash_attn_bwd_acc_split(int(seqlen)))
+
+
+def set_acc_split(w: int):
+    """dash_attn_bwd_set_acc_split (host-global)."""
+    _check(_lib.dash_attn_bwd_set_acc_split(int(w)), "dash_attn_bwd_set_acc_split")
 
 
 def attn_bwd_dump(q, k, v, o, dout, lse, causal: bool, schedule, deterministic=True, scale=None,

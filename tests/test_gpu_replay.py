@@ -7,8 +7,10 @@ dQ tile's partials in the order the paper prescribes -- the ranks come from
 oracle/dag_oracle.reduction_ranks, built from the paper's schedule
 definitions (AMB-6), not from the product's tables --
 with one IEEE fp32 round-to-nearest add per contribution (Alg.1 line 34,
-P:396), then applies dq = bf16_rn(scale * sum) (AMB-14).  The GPU's fp32
-accumulator and its dq must match those bits exactly.  A wrong rank,
+P:396), then applies dq = bf16_rn(scale * sum) (AMB-14).  With W interleaved
+accumulators (AMB-27) each accumulator w re-sums ranks w, w + W, ... and the
+convert adds them in index order.  The GPU's fp32 accumulators and its dq must
+match those bits exactly.  A wrong rank,
 a skipped or doubled contribution, an add that raced its predecessor, or a
 scale applied per partial all change bits.
 """
@@ -38,11 +40,20 @@ def bf16_rn_bits(x32: np.ndarray) -> np.ndarray:
     return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
 
 
+@pytest.fixture(params=[1, 2, 4], ids=lambda w: f"W{w}")
+def acc_split(request, dash):
+    """Run the test under W interleaved accumulators (AMB-27), then restore."""
+    old = dash.acc_split()
+    dash.set_acc_split(request.param)
+    yield request.param
+    dash.set_acc_split(old)
+
+
 @pytest.mark.parametrize("N", [512, 384])
 @pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("schedule", ["naive", "descending", "shift"])
-def test_dq_equals_host_resum_in_paper_order(dash, N, d, causal, schedule):
+def test_dq_equals_host_resum_in_paper_order(dash, acc_split, N, d, causal, schedule):
     B, H = 1, 2
     T = 128                                                # schedule tile rows (AMB-11)
     n = N // T
@@ -56,7 +67,9 @@ def test_dq_equals_host_resum_in_paper_order(dash, N, d, causal, schedule):
                                                schedule, True)
     torch.cuda.synchronize()
     parts = parts.cpu().numpy()                                        # [B*H, N/128, N, d] fp32
-    acc_gpu = ws[: B * H * N * d * 4].view(torch.float32).cpu().numpy().reshape(B * H, N, d)
+    W = acc_split                                                      # AMB-27
+    assert dash.acc_split(N) == W
+    acc_gpu = ws[: W * B * H * N * d * 4].view(torch.float32).cpu().numpy().reshape(W, B * H, N, d)
     dq_bits = dq.view(torch.int16).cpu().numpy().view(np.uint16)     # [B, N, H, d]
     scale = np.float32(1.0) / np.sqrt(np.float32(d))
     rank = dag.reduction_ranks(sched, n, mask)
@@ -72,12 +85,20 @@ def test_dq_equals_host_resum_in_paper_order(dash, N, d, causal, schedule):
             order = sorted((rk, i) for (i, jj), rk in rank.items() if jj == j)
             assert [rk for rk, _ in order] == list(range(len(order)))
             rows = slice(j * T, (j + 1) * T)
-            acc = contribution(bh, order[0][1], j).copy()     # rank 0 stores
-            for _, i in order[1:]:                             # ranks 1.. add, in order
-                acc = (acc + contribution(bh, i, j)).astype(np.float32)
-            np.testing.assert_array_equal(acc_gpu[bh, rows].view(np.uint32), acc.view(np.uint32),
-                                          err_msg=f"dQacc bh={bh} tile={j}")
+            accs = []
+            for w in range(min(W, len(order))):
+                # accumulator w: ranks w, w + W, ... in order; its first one stores
+                mine = [i for rk, i in order if rk % W == w]
+                acc = contribution(bh, mine[0], j).copy()
+                for i in mine[1:]:
+                    acc = (acc + contribution(bh, i, j)).astype(np.float32)
+                np.testing.assert_array_equal(acc_gpu[w, bh, rows].view(np.uint32), acc.view(np.uint32),
+                                              err_msg=f"dQacc[{w}] bh={bh} tile={j}")
+                accs.append(acc)
             checked_acc += len(order) >= 2
+            acc = accs[0]
+            for extra in accs[1:]:                              # convert: acc_0 + acc_1
+                acc = (acc + extra).astype(np.float32)
             want = bf16_rn_bits((acc * scale).astype(np.float32))
             got = dq_bits[b, rows, h, :]
             bad = np.count_nonzero(got != want)
