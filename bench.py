@@ -291,7 +291,8 @@ def main():
     ap.add_argument("--impl", default="dash", choices=["dash", "reference"])
     ap.add_argument("--head-dim", type=int, default=128)
     ap.add_argument("--full", action="store_true", help="full mask instead of causal")
-    ap.add_argument("--schedule", default=None)
+    ap.add_argument("--schedule", default=None,
+                    help="naive | descending | shift | auto (default: auto, the library's per-shape choice)")
     ap.add_argument("--acc-split", type=int, default=None,
                     help="interleaved dQ accumulators W in {1,2,4} (AMB-27); default: the library's automatic choice")
     ap.add_argument("--no-sweep", action="store_true", help="skip the per-schedule sweep table")
@@ -302,7 +303,7 @@ def main():
     args = ap.parse_args()
     causal = not args.full
     if args.schedule is None:
-        args.schedule = "shift"
+        args.schedule = "auto"
     if args.impl == "reference":
         bench_reference(args)
         return
@@ -394,7 +395,8 @@ def main():
         sweep = []
         w_bench = dash.acc_split()
         for s, g in probs:
-            row = {"seqlen": s[1], "batch": s[0], "heads": s[2], "acc_split": dash.acc_split(s[1])}
+            row = {"seqlen": s[1], "batch": s[0], "heads": s[2], "acc_split": dash.acc_split(s[1]),
+                   "auto": dash.resolve_schedule(s, causal, "auto")}
             f = fa_flops(*s, causal)
             cases = [("naive", "naive", True, w_bench), ("descending", "descending", True, w_bench),
                      ("shift", "shift", True, w_bench), ("atomic", "naive", False, w_bench)]
@@ -437,7 +439,10 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded N(0,1) bf16 q,k,v,dO; O, L from dash_attn_fwd)",
-            "config": workload_config(args, world),
+            "config": dict(workload_config(args, world),
+                           schedule_resolved={str(sh[1]): dash.resolve_schedule(sh, causal, args.schedule)
+                                              for sh, _ in probs},
+                           acc_split_resolved={str(sh[1]): dash.acc_split(sh[1]) for sh, _ in probs}),
             "frac_of_peak": value / peak,
             "roofline": roofline,
             "cpu_baseline": cpu,

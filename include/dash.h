@@ -61,7 +61,10 @@ typedef enum { DASH_MASK_FULL = 0, DASH_MASK_CAUSAL = 1 } dash_mask;
 typedef enum {
   DASH_SCHED_NAIVE = 0,
   DASH_SCHED_DESCENDING = 1,
-  DASH_SCHED_SHIFT = 2
+  DASH_SCHED_SHIFT = 2,
+  /* dash_attn_bwd only: one of the three above, chosen per (mask, N, d) --
+   * see dash_attn_bwd_resolve_schedule. */
+  DASH_SCHED_AUTO = 3
 } dash_schedule;
 
 typedef struct {
@@ -186,6 +189,13 @@ dash_status dash_attn_bwd_trace(const dash_shape* shape, const void* q, const vo
                                 void* dq, void* dk, void* dv, int causal, int schedule,
                                 int deterministic, void* workspace, size_t workspace_bytes,
                                 unsigned long long* trace, int trace_cap, void* stream);
+
+/* The schedule dash_attn_bwd runs for `schedule` (DASH_SCHED_AUTO resolved,
+ * others returned unchanged): with n = N / 128, SHIFT for n <= 32; causal
+ * DESCENDING for n >= 64 at d = 128 and n >= 128 at d = 64 (SHIFT between);
+ * full mask NAIVE for n > 32 -- the fastest of the paper's three measured on
+ * B200.  Returns -1 for an invalid shape or schedule. */
+int dash_attn_bwd_resolve_schedule(const dash_shape* shape, int causal, int schedule);
 
 /* Number W of interleaved fp32 dQ accumulators the deterministic backward
  * uses (AMB-27).  W = 1 is the paper's single global order per dQ tile

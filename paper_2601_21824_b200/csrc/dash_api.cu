@@ -33,6 +33,20 @@ int g_acc_split = [] {
   return (v == 1 || v == 2 || v == 4) ? v : 0;
 }();
 int acc_split() { return g_acc_split; }
+// DASH_SCHED_AUTO: the paper's schedule that measured fastest on B200 for
+// this (mask, n, d) with the automatic accumulator split (bench sweeps in
+// profiles/README.md): SHIFT while heads are short (n <= 32 tiles: whole heads
+// fit the 148 SMs several times over); for longer causal heads DESCENDING
+// (d = 128 from n = 64, d = 64 from n = 128), for longer full-mask heads
+// NAIVE, whose dependencies all point to earlier-claimed jobs, so partially
+// co-scheduled heads never stall (with W = 4 its remaining chain cost is gone).
+int auto_schedule(const dash_shape* s, int causal) {
+  const int n = s->seqlen / 128;
+  if (n <= 32) return kShift;
+  if (causal) return (n >= 128 || (s->head_dim == 128 && n >= 64)) ? kDescending : kShift;
+  return kNaive;
+}
+
 // W actually used for a problem with n 128-row tiles per head.  Automatic:
 // W = 4 once the per-tile chain is long (n >= 64), else 2 -- measured on
 // B200 (profiles/r01_experiments/acc_split.txt): extra accumulators cost the
@@ -406,8 +420,9 @@ DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const voi
   const void* ptrs[] = {q, k, v, o, dout, lse, dq, dk, dv, workspace};
   for (const void* p : ptrs)
     if (!aligned16(p)) return DASH_ERR_INVALID_ARG;
-  if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_SHIFT) return DASH_ERR_INVALID_ARG;
+  if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_AUTO) return DASH_ERR_INVALID_ARG;
   if (workspace_bytes < ws_layout(s).total) return DASH_ERR_WORKSPACE;
+  if (schedule == DASH_SCHED_AUTO) schedule = auto_schedule(s, causal);
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   // smem variant (BwdCfg): DASH_VARIANT overrides the default (experiments)
   static const int variant = [] {
@@ -454,6 +469,11 @@ DASH_API dash_status dash_attn_bwd_set_acc_split(int w) {
 DASH_API size_t dash_attn_bwd_dump_bytes(const dash_shape* s) {
   if (!shape_ok(s)) return 0;
   return static_cast<size_t>(s->batch) * s->heads * (s->seqlen / 128) * s->seqlen * s->head_dim * 4;
+}
+
+DASH_API int dash_attn_bwd_resolve_schedule(const dash_shape* s, int causal, int schedule) {
+  if (!shape_ok(s) || schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_AUTO) return -1;
+  return schedule == DASH_SCHED_AUTO ? auto_schedule(s, causal) : schedule;
 }
 
 DASH_API dash_status dash_attn_bwd_dump(const dash_shape* s, const void* q, const void* k,

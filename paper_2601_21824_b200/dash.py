@@ -15,9 +15,9 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdash.so")
 
-NAIVE, DESCENDING, SHIFT = 0, 1, 2
+NAIVE, DESCENDING, SHIFT, AUTO = 0, 1, 2, 3
 FULL, CAUSAL = 0, 1
-SCHEDULES = {"naive": NAIVE, "descending": DESCENDING, "shift": SHIFT}
+SCHEDULES = {"naive": NAIVE, "descending": DESCENDING, "shift": SHIFT, "auto": AUTO}
 
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_WORKSPACE, ERR_CUDA, ERR_DEADLOCK = range(6)
 
@@ -57,6 +57,8 @@ def _load():
     lib.dash_attn_bwd_trace.restype = st
     lib.dash_attn_bwd_trace.argtypes = [SP, vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp, sz,
                                         vp, i, vp]
+    lib.dash_attn_bwd_resolve_schedule.restype = i
+    lib.dash_attn_bwd_resolve_schedule.argtypes = [SP, i, i]
     lib.dash_attn_bwd_acc_split.restype = i
     lib.dash_attn_bwd_acc_split.argtypes = [i]
     lib.dash_attn_bwd_set_acc_split.restype = st
@@ -183,6 +185,16 @@ def attn_bwd_trace(q, k, v, o, dout, lse, causal: bool, schedule, deterministic,
                                     workspace.numel(), _ptr(trace), trace_cap, _stream(q)),
            "dash_attn_bwd_trace")
     return (dq, dk, dv), trace
+
+
+def resolve_schedule(shape_bnhd, causal: bool, schedule) -> str:
+    """dash_attn_bwd_resolve_schedule: the paper schedule `schedule` runs as."""
+    B, N, H, d = shape_bnhd
+    shp = Shape(B, N, H, d, 0.0)
+    r = int(_lib.dash_attn_bwd_resolve_schedule(ctypes.byref(shp), int(causal), _sched(schedule)))
+    if r < 0:
+        raise DashError(ERR_INVALID_ARG, "dash_attn_bwd_resolve_schedule")
+    return {NAIVE: "naive", DESCENDING: "descending", SHIFT: "shift"}[r]
 
 
 def acc_split(seqlen: int = 0) -> int:

@@ -143,3 +143,32 @@ def test_bwd_rejects_bad_arguments_without_gpu(dash):
     bad = dash.Shape(1, 200, 1, 64, 0.0)
     st = lib.dash_attn_bwd(ctypes.byref(bad), *args, 0, 0, 1, p, 1 << 30, nul)
     assert st == dash.ERR_INVALID_ARG
+
+
+def test_auto_schedule_policy_and_acc_split(dash):
+    """DASH_SCHED_AUTO resolves to one of the paper's three schedules by the
+    documented rule (include/dash.h); the automatic accumulator split depends
+    on N only (AMB-27), so (b, h) sharding can never change it."""
+    cases = [  # (N, d, causal) -> schedule
+        ((512, 128, True), "shift"), ((4096, 128, True), "shift"), ((8192, 128, True), "descending"),
+        ((16384, 128, True), "descending"), ((8192, 64, True), "shift"), ((16384, 64, True), "descending"),
+        ((4096, 128, False), "shift"), ((8192, 128, False), "naive"), ((16384, 64, False), "naive"),
+    ]
+    for (N, d, causal), want in cases:
+        assert dash.resolve_schedule((1, N, 16, d), causal, "auto") == want, (N, d, causal)
+        for b, h in ((8, 32), (1, 1)):  # independent of B and H
+            assert dash.resolve_schedule((b, N, h, d), causal, "auto") == want
+        assert dash.resolve_schedule((1, N, 16, d), causal, "naive") == "naive"
+    old = dash.acc_split()
+    try:
+        dash.set_acc_split(0)
+        assert [dash.acc_split(N) for N in (512, 4096, 8192, 32768)] == [2, 2, 4, 4]
+        for w in (1, 2, 4):
+            dash.set_acc_split(w)
+            assert dash.acc_split(1024) == w and dash.acc_split() == w
+        with pytest.raises(dash.DashError):
+            dash.set_acc_split(3)
+    finally:
+        dash.set_acc_split(old)
+    with pytest.raises(dash.DashError):  # AUTO is not a schedule of the DAG model
+        dash.schedule_critical_path(dash.AUTO, 4, 4, dash.CAUSAL)

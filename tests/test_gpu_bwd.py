@@ -211,3 +211,15 @@ def test_full_size_sampled_kv_rows(dash):
         gv = dv[b, cols, h].float().cpu().numpy()
         assert np.max(np.abs(gk - rk[a])) / np.max(np.abs(rk[a])) <= GRAD_TOL
         assert np.max(np.abs(gv - rv[a])) / np.max(np.abs(rv[a])) <= GRAD_TOL
+
+
+@pytest.mark.parametrize("N,causal", [(512, True), (1024, False)])
+def test_auto_schedule_runs_the_resolved_schedule(dash, N, causal):
+    """DASH_SCHED_AUTO gives exactly the bits of the schedule it resolves to."""
+    B, H, d = 1, 4, 128
+    _, g = _inputs(B, N, H, d, seed=6)
+    want = dash.resolve_schedule((B, N, H, d), causal, "auto")
+    _, _, *a = _run(dash, g, causal, "auto", True)
+    _, _, *b = _run(dash, g, causal, want, True)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
