@@ -20,9 +20,10 @@
 // Warp roles (16 warps, 512 threads):
 //   0      TMA producer (K/V per KV tile, Q/dO/L/D per sub-tile, NSTAGE ring)
 //   1      MMA issuer (one thread) + TMEM owner
-//   2, 3   dQ reducers: lane 0 of warp 2 handles even sub-tiles, of warp 3
-//          odd ones (acquire ticket -> TMA reduce-add -> wait -> release), so
-//          two ordered adds are in flight; warp 2 also claims jobs
+//   2, 3   dQ reducers: one single-thread agent per warp (lane 0); staging
+//          unit x belongs to agent x % 2 (acquire ticket -> bulk reduce-add ->
+//          read done frees the staging -> completion -> release), so two
+//          ordered adds are in flight; agent 0 also claims jobs
 //   4-11   softmax / dS, then the dK/dV epilogue: two warpgroups, each owning
 //          half of the sub-tile's columns (TMEM lane quarter = warp % 4)
 //   12-15  dQ drain: TMEM -> registers -> SW128 fp32 staging
@@ -62,6 +63,7 @@ struct BwdArgs {
   // accumulators in index order.  W = 1 is the paper's single global order.
   int split;
   int n_tickets;  // tickets per accumulator
+  float* dqacc;   // the accumulators (1-D bulk reduce variant, V = 3)
 };
 
 // Per-(CTA, sub-tile) clock64 stamps for pipeline analysis; a null trace
@@ -80,7 +82,12 @@ struct BwdArgs {
 //        while the previous one still waits for its ticket), ring of 2;
 // V = 2: the partial staged and reduced in two halves of BR/2 rows, each with
 //        its own ticket (two shorter hand-offs per sub-tile), one half-size
-//        buffer per reducer, same ring as V = 0.
+//        buffer per reducer, same ring as V = 0;
+// V = 3: as V = 0, but d = 128 partials are staged row-major (linear) and
+//        reduced with 1-D bulk copies (cp.reduce.async.bulk, no tensor map):
+//        a sub-tile's partial is one contiguous 32 KB run of dQacc.  The
+//        buffer is a ring of two halves (rows 0-31, 32-63): the drain writes
+//        one half while the bulk engine still reads the other.
 template <int D, int V = 0>
 struct BwdCfg {
   static constexpr int NTHREADS = 512;
@@ -88,7 +95,8 @@ struct BwdCfg {
   static constexpr int BR = (D == 128) ? 64 : 128;  // Q sub-tile rows
   static constexpr int NSUB = 128 / BR;             // sub-tiles per schedule Q tile
   static constexpr int NSTAGE = (D == 128 && V != 1) ? 3 : 2;  // Q/dO/L/D ring depth
-  static constexpr int NSTG = V ? 2 : 1;                       // dQ staging buffers
+  static constexpr int NSTG = (V == 1 || V == 2) ? 2 : 1;     // dQ staging buffers
+  static constexpr bool LINEAR = (V == 3 && D == 128);         // 1-D bulk reduce of a linear tile
   static constexpr int NSMX = 2;                    // softmax warpgroups (column halves)
   static constexpr int SMX_COLS = BR / NSMX;        // columns per softmax thread
   static constexpr uint32_t KV_BYTES = BC * D * 2;
@@ -115,7 +123,7 @@ struct BwdCfg {
   static constexpr uint32_t OFF_L = OFF_DQ + NSTG * DQ_BYTES;    // NSTAGE x BR floats
   static constexpr uint32_t OFF_DV = OFF_L + NSTAGE * BR * 4;    // NSTAGE x BR floats
   static constexpr uint32_t OFF_BAR = OFF_DV + NSTAGE * BR * 4;
-  static constexpr int NBAR = 32;
+  static constexpr int NBAR = 40;
   static constexpr uint32_t OFF_MISC = OFF_BAR + NBAR * 8;
   static constexpr uint32_t BODY_BYTES = OFF_MISC + 64;
   // Re-alignment slack for the 1024-B swizzle atoms (as much as fits; the
@@ -148,12 +156,14 @@ enum : int {
   B_DS_EMPTY0 = 22, B_DS_EMPTY1 = 23,  // dS^T smem buffer consumed by dK, dQ (commit)
   B_ACC_FULL = 12, B_ACC_EMPTY = 13,   // dK/dV complete (commit) / drained (256)
   B_STG_EMPTY = 14,                    // staging (buffer 0) read by the reduce (1)
-  B_JOB_DONE = 15,                     // both reducers released the job (2)
-  B_STG_FULL0 = 16, B_STG_FULL1 = 17,  // staging written, for reducer x & 1 (128)
+  B_JOB_DONE = 15,                     // every reducer agent released the job (NAG)
   B_Q_FULL0 = 18,                      // + stage (<= 4): Q/dO/L/D loaded (tx)
   B_Q_EMPTY0 = 26,                     // + stage (<= 4): stage consumed (commit)
-  B_COUNT = 30
+  B_AGF0 = 32,                         // + h * NAG + agent: staging (half h) written for
+                                       // the agent of unit x (x % NAG) (128)
+  B_COUNT = 40
 };
+constexpr int NAG = 2;  // reducer agents (single threads, one per reducer warp)
 
 __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -224,9 +234,8 @@ __global__ void __launch_bounds__(512, 1)
     ptx::mbar_init(&bars[B_P_FULL], 128 * C::NSMX);
     ptx::mbar_init(&bars[B_ACC_EMPTY], 128 * C::NSMX);
     ptx::mbar_init(&bars[B_DQ_EMPTY], 128);
-    ptx::mbar_init(&bars[B_STG_FULL0], 128);
-    ptx::mbar_init(&bars[B_STG_FULL1], 128);
-    ptx::mbar_init(&bars[B_JOB_DONE], 2);
+    for (int i = 0; i < 2 * NAG; ++i) ptx::mbar_init(&bars[B_AGF0 + i], 128);
+    ptx::mbar_init(&bars[B_JOB_DONE], NAG);
     ptx::fence_mbar_init();
     ptx::fence_async_smem();
     ptx::prefetch_tmap(&tm_q);
@@ -391,11 +400,16 @@ __global__ void __launch_bounds__(512, 1)
     }
   } else if (warp == 2 || warp == 3) {
     // ======================== ordered dQ reducers ==========================
-    {  // whole warp converged; one elected lane owns the bulk groups
-      const uint32_t rid = static_cast<uint32_t>(warp - 2);
+    // NAG = 2 single-thread agents (lane 0 of warps 2 and 3), each with its
+    // own bulk groups; staging unit x belongs to agent x % NAG, so two ordered
+    // adds are in flight.  (Measured: four agents as lanes 0 and 16 of the
+    // same two warps are slower -- divergent lanes of one warp do not run
+    // concurrently, so a spinning agent stalls its lane-mate.)
+    if (lane == 0) {
+      const uint32_t agent = static_cast<uint32_t>(warp - 2);
       const bool det = args.deterministic != 0;
       uint32_t it_job = 0, x = 0;
-      if (rid == 0 && lane == 0) {
+      if (agent == 0) {
         job_slot[0] = atomicAdd(args.job_counter, 1);
         ptx::mbar_arrive(&bars[B_JOB0]);
       }
@@ -409,7 +423,8 @@ __global__ void __launch_bounds__(512, 1)
           const int q = tk.x >> 16, rank = tk.y;
           for (int sub = 0; sub < NSUB; ++sub) {
            for (int h = 0; h < C::NUNIT; ++h, ++x) {  // x counts staging units here
-            if ((x & 1) != rid) continue;
+            if ((x % NAG) != agent) continue;
+            const uint32_t ph = (x / NAG) & 1;  // this agent's phase on its FULL barriers
             const int urow = q * 128 + sub * BR + h * C::STG_ROWS;  // first Q row of the unit
             const int par = rank % args.split, rank_w = rank / args.split;  // AMB-27
             int* ticket = args.tickets + static_cast<size_t>(par) * args.n_tickets +
@@ -424,28 +439,42 @@ __global__ void __launch_bounds__(512, 1)
                   __nanosleep(32);
                   if (clock64() - t_start > 8 * ptx::kWatchdogCycles ||
                       *reinterpret_cast<volatile int*>(&ptx::g_dash_abort)) {  // ~35 s bound
-                    if (lane == 0) {
-                      atomicExch(args.error_flag, 1);
-                      atomicExch(&ptx::g_dash_abort, 1);
-                    }
+                    atomicExch(args.error_flag, 1);
+                    atomicExch(&ptx::g_dash_abort, 1);
                     break;
                   }
                 }
                 (void)ptx::ld_acquire(ticket);
               }
+              // Order the ticket acquire (generic proxy) before the reduce (async proxy).
+              ptx::fence_async_global();
             }
-            // Order the ticket acquire (generic proxy) before the reduce (async
-            // proxy); done while the partial is still being staged.
-            if (det) ptx::fence_async_global();
-            if (lane == 0 && h == 0) DASH_TRACE_MARK(7, x / C::NUNIT);
-            // one barrier per reducer: never test a parity two phases ahead
-            if (!(args.debug & 4)) ptx::mbar_wait(&bars[B_STG_FULL0 + rid], (x >> 1) & 1);
-            __syncwarp();
+            if (h == 0) DASH_TRACE_MARK(7, x / C::NUNIT);
             // Add dQ_local to dQ (Alg.1 line 34); rank 0 stores (no zero-fill needed).
             // row of dQacc [W][B*H*N, D]
             const int grow = (par * args.B * args.H + jv.bh) * args.N + urow;
             const uint8_t* stg = smem + C::OFF_DQ + (x % NSTG) * C::DQ_BYTES;
-            if (lane == 0) {
+            if constexpr (C::LINEAR) {
+              // two halves; the second may still be in the drain's hands
+              float* dst0 = args.dqacc + static_cast<size_t>(grow) * D;
+              constexpr uint32_t HB = C::DQ_BYTES / 2;
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                if (!(args.debug & 4)) ptx::mbar_wait(&bars[B_AGF0 + hh * NAG + agent], ph);
+                if (!(args.debug & 1)) {
+                  float* dst = dst0 + hh * (HB / 4);
+                  if (det && rank_w == 0) ptx::bulk_store(dst, stg + hh * HB, HB);
+                  else ptx::bulk_reduce_add_f32(dst, stg + hh * HB, HB);
+                }
+                ptx::bulk_commit();
+              }
+              if (h == 0) DASH_TRACE_MARK(8, x / C::NUNIT);
+              ptx::bulk_wait_read<1>();  // first half read: the drain may refill it
+              ptx::mbar_arrive(&bars[B_STG_EMPTY]);
+              ptx::bulk_wait_read<0>();
+              ptx::mbar_arrive(&bars[B_STG_EMPTY1]);
+            } else {
+              if (!(args.debug & 4)) ptx::mbar_wait(&bars[B_AGF0 + agent], ph);
 #pragma unroll
               for (int blk = 0; blk < D / 32; ++blk) {
                 if (args.debug & 1) break;  // timing experiment: no reduce traffic
@@ -459,38 +488,35 @@ __global__ void __launch_bounds__(512, 1)
               if (h == 0) DASH_TRACE_MARK(8, x / C::NUNIT);
               ptx::bulk_wait_read_all();  // staging may be overwritten from here on
               ptx::mbar_arrive(stg_empty(x));
-              if (h == 0) DASH_TRACE_MARK(11, x / C::NUNIT);
-              ptx::bulk_wait_all();
-              if (h == 0) DASH_TRACE_MARK(12, x / C::NUNIT);
-              if (det) {
-                // Advance the global order (Alg.1 line 35): proxy fence (the
-                // reduce wrote through the async proxy) + gpu-scope release.
-                // Measured: a relaxed store here is NOT safe -- completion of
-                // the bulk group alone does not order the reduce's writes
-                // before the flag (tests/test_gpu_bwd.py catches it).
-                ptx::fence_async_global();
-                ptx::st_release(ticket, rank_w + 1);
-              }
-              if (h == C::NUNIT - 1) DASH_TRACE_MARK(9, x / C::NUNIT);
             }
-            __syncwarp();
+            if (h == 0) DASH_TRACE_MARK(11, x / C::NUNIT);
+            ptx::bulk_wait_all();
+            if (h == 0) DASH_TRACE_MARK(12, x / C::NUNIT);
+            if (det) {
+              // Advance the global order (Alg.1 line 35): proxy fence (the
+              // reduce wrote through the async proxy) + gpu-scope release.
+              // Measured: a relaxed store here is NOT safe -- completion of
+              // the bulk group alone does not order the reduce's writes
+              // before the flag (tests/test_gpu_bwd.py catches it).
+              ptx::fence_async_global();
+              ptx::st_release(ticket, rank_w + 1);
+            }
+            if (h == C::NUNIT - 1) DASH_TRACE_MARK(9, x / C::NUNIT);
            }
           }
         }
-        // Both reducers have released every add of this job: only now may the
+        // Every agent has released every add of this job: only now may the
         // CTA claim its next job (greedy claiming of AMB-7, deadlock-free).
-        if (lane == 0) ptx::mbar_arrive(&bars[B_JOB_DONE]);
-        if (rid == 0) {
+        ptx::mbar_arrive(&bars[B_JOB_DONE]);
+        if (agent == 0) {
           ptx::mbar_wait(&bars[B_JOB_DONE], it_job & 1);
-          if (lane == 0) {
-            job_slot[(it_job + 1) & 1] = atomicAdd(args.job_counter, 1);
-            ptx::mbar_arrive(&bars[B_JOB0 + ((it_job + 1) & 1)]);
-          }
+          job_slot[(it_job + 1) & 1] = atomicAdd(args.job_counter, 1);
+          ptx::mbar_arrive(&bars[B_JOB0 + ((it_job + 1) & 1)]);
         }
-        __syncwarp();
         ++it_job;
       }
     }
+    __syncwarp();
   } else if (warp >= 4 && warp < 4 + 4 * C::NSMX) {
     // ======================= softmax / dS / epilogue ======================
     const int wg = (warp - 4) >> 2;          // column half owned by this warpgroup
@@ -652,6 +678,20 @@ __global__ void __launch_bounds__(512, 1)
         for (int h = 0; h < C::NUNIT; ++h) {
           const uint32_t y = x * C::NUNIT + h;  // staging unit
           if (args.debug & 4) continue;  // timing experiment: no staging (pure compute pipeline)
+          if constexpr (C::LINEAR) {
+            // row-major [STG_ROWS][128] fp32 in two halves; lane tl = d index, v[c] = Q row c
+            constexpr int HR = C::STG_ROWS / 2;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              if (y >= 1) ptx::mbar_wait(&bars[hh ? B_STG_EMPTY1 : B_STG_EMPTY], (y - 1) & 1);
+#pragma unroll
+              for (int c = hh * HR; c < (hh + 1) * HR; ++c)
+                reinterpret_cast<float*>(stg0)[c * 128 + tl] = v[h * C::STG_ROWS + c];
+              ptx::fence_async_smem();
+              ptx::mbar_arrive(&bars[B_AGF0 + hh * NAG + (y % NAG)]);
+            }
+            continue;
+          }
           if (y >= NSTG) ptx::mbar_wait(stg_empty(y), ((y / NSTG) - 1) & 1);
           uint8_t* stg = stg0 + (y % NSTG) * C::DQ_BYTES;
           // Stage STG_ROWS rows of the fp32 partial as SW128 boxes of 32 columns.
@@ -678,7 +718,7 @@ __global__ void __launch_bounds__(512, 1)
             }
           }
           ptx::fence_async_smem();
-          ptx::mbar_arrive(&bars[B_STG_FULL0 + (y & 1)]);
+          ptx::mbar_arrive(&bars[B_AGF0 + (y % NAG)]);
         }
         if (tl == 0) DASH_TRACE_MARK(6, x);
       }

@@ -24,7 +24,7 @@ namespace dash {
 namespace {
 
 constexpr size_t kAlign = 1024;
-constexpr int kDefaultVariant = 0;  // BwdCfg smem variant used unless DASH_VARIANT is set
+constexpr int kDefaultVariant = 3;  // BwdCfg smem variant used unless DASH_VARIANT is set
 // Interleaved dQ accumulators (AMB-27): 0 = automatic (the default), else
 // fixed W in {1, 2, 4}; DASH_ACC_SPLIT overrides the default at load time.
 int g_acc_split = [] {
@@ -283,6 +283,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     a.trace_cap = g_trace_cap;
     a.debug = debug_bits;
     a.split = deterministic ? acc_split_for(n) : 1;
+    a.dqacc = dqacc;
     a.n_tickets = static_cast<int>(w.n_tickets);
     a.dump = g_dump;
     auto kern = dash_bwd_kernel<D, V>;
@@ -434,7 +435,10 @@ DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const voi
   launch_bwd<DD, VV>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule, deterministic, \
                      workspace, st)
   if (s->head_dim == 128)
-    return var == 2 ? DASH_LAUNCH(128, 2) : var == 1 ? DASH_LAUNCH(128, 1) : DASH_LAUNCH(128, 0);
+    return var == 3   ? DASH_LAUNCH(128, 3)
+           : var == 2 ? DASH_LAUNCH(128, 2)
+           : var == 1 ? DASH_LAUNCH(128, 1)
+                      : DASH_LAUNCH(128, 0);
   return var == 2 ? DASH_LAUNCH(64, 2) : var == 1 ? DASH_LAUNCH(64, 1) : DASH_LAUNCH(64, 0);
 #undef DASH_LAUNCH
 }

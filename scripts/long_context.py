@@ -34,9 +34,11 @@ def main():
     out = tuple(torch.empty_like(g["q"]) for _ in range(3))
     flops = 10.0 * B * H * N * N * d / 2
     res = {"config": "long-context", "B": B, "N": N, "H": H, "d": d, "mask": "causal",
-           "flops_fa_convention": flops}
+           "flops_fa_convention": flops, "acc_split": dash.acc_split(N),
+           "auto_schedule": dash.resolve_schedule((B, N, H, d), True, "auto")}
     for name, sched, det in (("naive", "naive", True), ("descending", "descending", True),
-                             ("shift", "shift", True), ("atomic", "naive", False)):
+                             ("shift", "shift", True), ("atomic", "naive", False),
+                             ("auto", "auto", True)):
         dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, True, sched, det, workspace=ws,
                       out=out)
         torch.cuda.synchronize()
@@ -49,13 +51,13 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.reps
         res[name] = {"ms": ms, "tflops": flops / (ms / 1e3) / 1e12}
-        if name == "shift":
+        if name == "auto":
             dq = out[0]
             f = {k: v[:1].double().numpy() for k, v in cpu.items()}  # batch 0 only
             heads, rows = [0, 31], [0, 4097, 20000, 32767]
             ref = oracle.attn_bwd_dq_rows(f["q"], f["k"], f["v"], f["do"], True, heads, rows)
             got = np.stack([dq[0, rows, h].float().cpu().numpy() for h in heads])
-            res["shift"]["sampled_dq_err_normalised"] = float(
+            res["auto"]["sampled_dq_err_normalised"] = float(
                 np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
     res["deadlock_check"] = dash.check_workspace(g["q"].shape, True, "shift", True, ws)
     gap = res["atomic"]["tflops"] - res["naive"]["tflops"]

@@ -66,7 +66,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--ns", default="4,8,16,32,64,128")
+    ap.add_argument("--acc-split", type=int, default=1,
+                    help="W (AMB-27); the DAG model is the paper's single chain, W = 1")
     args = ap.parse_args()
+    dash.set_acc_split(args.acc_split)
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     rows = []
     for n in (int(v) for v in args.ns.split(",")):
@@ -80,6 +83,7 @@ def main():
             mask = dash.CAUSAL if causal else dash.FULL
             m = B * H
             row = {"n": n, "N": N, "B": B, "H": H, "mask": "causal" if causal else "full",
+                   "acc_split": dash.acc_split(N),
                    "c_cycles": c, "r_cycles": r, "n_sm": sms, "heads_m": m}
             t_naive = time_bwd(g, causal, "naive")
             cp_naive = dash.schedule_critical_path(dash.NAIVE, n, n, mask, m, sms, c, r)
