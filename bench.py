@@ -48,6 +48,7 @@ SEQLENS = (512, 1024, 2048, 4096, 8192, 16384)
 TOKENS, HIDDEN = 16384, 2048
 METRIC = "deterministic attn-bwd TFLOPs/s vs atomic bwd; % of B200 BF16 tensor peak"
 CPU_SAMPLE_N = 2048  # sweep point used for the oracle's bounded sample
+SWEEP_ROUNDS = 3     # interleaved timing rounds of the per-schedule table (median)
 
 
 def fa_flops(B, N, H, d, causal):
@@ -403,15 +404,25 @@ def main():
             if dash.acc_split(s[1]) != 1:
                 cases += [("naive_w1", "naive", True, 1), ("descending_w1", "descending", True, 1),
                           ("shift_w1", "shift", True, 1)]
-            for name, sched, det, w in cases:
-                dash.set_acc_split(w)
-                try:
-                    t = time_steps(torch, lambda: run_bwd(dash, g, causal, sched, det),
-                                   max(3, args.steps), 2, 1)
-                    row[name] = f * max(3, args.steps) / (t / 1e3) / 1e12
-                except dash.DashError as e:
-                    row[name] = None
-                    row[name + "_error"] = str(e)
+            # Round-robin over the cases, SWEEP_ROUNDS times, median per case:
+            # every schedule sees the same clock / power history (a case timed
+            # right after a cool-down would otherwise be favoured).
+            times = {name: [] for name, *_ in cases}
+            nst = max(3, args.steps)
+            for _ in range(SWEEP_ROUNDS):
+                for name, sched, det, w in cases:
+                    if row.get(name + "_error"):
+                        continue
+                    dash.set_acc_split(w)
+                    try:
+                        times[name].append(time_steps(
+                            torch, lambda: run_bwd(dash, g, causal, sched, det), nst, 2, 1))
+                    except dash.DashError as e:
+                        row[name + "_error"] = str(e)
+            for name, *_ in cases:
+                row[name] = (f * nst / (statistics.median(times[name]) / 1e3) / 1e12
+                             if times[name] and not row.get(name + "_error") else None)
+            row["rounds"] = SWEEP_ROUNDS
             dash.set_acc_split(w_bench)
             for suffix in ("", "_w1"):
                 if row.get("naive" + suffix) is None:
