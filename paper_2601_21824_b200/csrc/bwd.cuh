@@ -64,6 +64,13 @@ struct BwdArgs {
   int split;
   int n_tickets;  // tickets per accumulator
   float* dqacc;   // the accumulators (1-D bulk reduce variant, V = 3)
+  // Early claim of the next job (see the producer): 0 = claim only after every
+  // ordered add of the current job is released; 1 = the producer claims the next
+  // job as soon as it has issued the current job's last load, when that is
+  // deadlock-free (cyclic = 1: the schedule has cyclic waits inside a head, so
+  // the next job must belong to another head).
+  int prefetch;
+  int cyclic;
 };
 
 // Per-(CTA, sub-tile) clock64 stamps for pipeline analysis; a null trace
@@ -87,7 +94,10 @@ struct BwdArgs {
 //        reduced with 1-D bulk copies (cp.reduce.async.bulk, no tensor map):
 //        a sub-tile's partial is one contiguous 32 KB run of dQacc.  The
 //        buffer is a ring of two halves (rows 0-31, 32-63): the drain writes
-//        one half while the bulk engine still reads the other.
+//        one half while the bulk engine still reads the other;
+// V = 4: as V = 3 with a ring of four quarters (16 rows, 8 KB each): a
+//        quarter is refilled as soon as the bulk engine has read it, so
+//        staging the next partial overlaps reading the previous one.
 template <int D, int V = 0>
 struct BwdCfg {
   static constexpr int NTHREADS = 512;
@@ -96,7 +106,8 @@ struct BwdCfg {
   static constexpr int NSUB = 128 / BR;             // sub-tiles per schedule Q tile
   static constexpr int NSTAGE = (D == 128 && V != 1) ? 3 : 2;  // Q/dO/L/D ring depth
   static constexpr int NSTG = (V == 1 || V == 2) ? 2 : 1;     // dQ staging buffers
-  static constexpr bool LINEAR = (V == 3 && D == 128);         // 1-D bulk reduce of a linear tile
+  static constexpr bool LINEAR = (V == 3 || V == 4) && D == 128;  // 1-D bulk reduce of a linear tile
+  static constexpr int NPART = (V == 4) ? 4 : 2;                // linear staging ring parts
   static constexpr int NSMX = 2;                    // softmax warpgroups (column halves)
   static constexpr int SMX_COLS = BR / NSMX;        // columns per softmax thread
   static constexpr uint32_t KV_BYTES = BC * D * 2;
@@ -159,7 +170,10 @@ enum : int {
   B_JOB_DONE = 15,                     // every reducer agent released the job (NAG)
   B_Q_FULL0 = 18,                      // + stage (<= 4): Q/dO/L/D loaded (tx)
   B_Q_EMPTY0 = 26,                     // + stage (<= 4): stage consumed (commit)
-  B_AGF0 = 32,                         // + h * NAG + agent: staging (half h) written for
+  B_STG_EMPTY2 = 16, B_STG_EMPTY3 = 17, // linear staging parts 2, 3 read (1), V = 4
+  B_PF0 = 24,                          // + (t - 1) % 2: producer's claim decision for job t (1)
+  B_SLOT_FREE0 = 30,                   // + j % 2: every warp has read job j's slot (16)
+  B_AGF0 = 32,                         // + h * NAG + agent: staging (part h) written for
                                        // the agent of unit x (x % NAG) (128)
   B_COUNT = 40
 };
@@ -218,8 +232,20 @@ __global__ void __launch_bounds__(512, 1)
   uint8_t* smem = smem_raw + pad;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   auto stg_empty = [&](uint32_t unit) { return &bars[(unit % NSTG) ? B_STG_EMPTY1 : B_STG_EMPTY]; };
+  // linear staging: barrier "part hh of the buffer has been read by the bulk engine"
+  auto part_empty = [&](int hh) {
+    return &bars[hh == 0 ? B_STG_EMPTY : hh == 1 ? B_STG_EMPTY1 : hh == 2 ? B_STG_EMPTY2 : B_STG_EMPTY3];
+  };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_MISC);
   int* job_slot = reinterpret_cast<int*>(smem + C::OFF_MISC + 8);  // [2]
+  volatile int* claim_mode = reinterpret_cast<volatile int*>(smem + C::OFF_MISC + 16);  // [2]
+  // Job j travels in slot j % 2; before slot j % 2 is rewritten for job j every
+  // warp must have read job j - 2 from it (a claimed-ahead job can be written
+  // while a lagging reducer agent has not yet started the previous job).
+  auto slot_read = [&](uint32_t j) { ptx::mbar_arrive(&bars[B_SLOT_FREE0 + (j & 1)]); };
+  auto wait_slot_free = [&](uint32_t j) {
+    if (j >= 2) ptx::mbar_wait(&bars[B_SLOT_FREE0 + (j & 1)], ((j - 2) >> 1) & 1);
+  };
   float* sL = reinterpret_cast<float*>(smem + C::OFF_L);
   float* sDv = reinterpret_cast<float*>(smem + C::OFF_DV);
 
@@ -234,8 +260,10 @@ __global__ void __launch_bounds__(512, 1)
     ptx::mbar_init(&bars[B_P_FULL], 128 * C::NSMX);
     ptx::mbar_init(&bars[B_ACC_EMPTY], 128 * C::NSMX);
     ptx::mbar_init(&bars[B_DQ_EMPTY], 128);
-    for (int i = 0; i < 2 * NAG; ++i) ptx::mbar_init(&bars[B_AGF0 + i], 128);
+    for (int i = 0; i < C::NPART * NAG; ++i) ptx::mbar_init(&bars[B_AGF0 + i], 128);
     ptx::mbar_init(&bars[B_JOB_DONE], NAG);
+    ptx::mbar_init(&bars[B_SLOT_FREE0], 16);
+    ptx::mbar_init(&bars[B_SLOT_FREE0 + 1], 16);
     ptx::fence_mbar_init();
     ptx::fence_async_smem();
     ptx::prefetch_tmap(&tm_q);
@@ -259,6 +287,7 @@ __global__ void __launch_bounds__(512, 1)
       while (true) {
         ptx::mbar_wait_u(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
         const int g = __shfl_sync(0xffffffffu, job_slot[it_job & 1], 0);
+        if (lane == 0) slot_read(it_job);
         ++it_job;
         if (g >= args.total_jobs || __shfl_sync(0xffffffffu, ptx::aborted(), 0)) break;
         const JobView jv = decode_job(args, g);
@@ -300,6 +329,44 @@ __global__ void __launch_bounds__(512, 1)
             ++q_cnt;
           }
         }
+        // Every load of job g is issued and (KV_EMPTY) every MMA of g has
+        // completed: claim the next job now -- its K/V load can start at once --
+        // instead of after the last ordered add of g is released (measured:
+        // that tail costs ~18 k cycles per job).  Claiming as soon as the loads
+        // are issued was slower: the claimed job then waits several sub-tiles,
+        // which splits the co-scheduling of a SHIFT head.  Deadlock-free: a CTA
+        // holds at most one claimed-ahead job, queued behind g; g's remaining
+        // adds wait only on jobs of g's head, all claimed earlier.  With cyclic
+        // waits inside a head (SHIFT) the claimed-ahead job must belong to
+        // another head, so it is never in g's wait cycle; with acyclic waits
+        // (NAIVE, DESCENDING: rank = KV index, waits point to earlier-claimed
+        // jobs) any job is fine.  Otherwise reducer agent 0 claims as before.
+        if (args.prefetch) ptx::mbar_wait_u(&bars[B_KV_EMPTY], (kv_cnt - 1) & 1);
+        if (lane == 0) {
+          int mode = 2;
+          wait_slot_free(it_job);  // slot it_job % 2 / claim_mode slot reusable
+          if (args.prefetch && !args.cyclic) {
+            job_slot[it_job & 1] = atomicAdd(args.job_counter, 1);
+            mode = 1;
+          } else if (args.prefetch) {
+            int peek = ptx::ld_relaxed(args.job_counter);
+            while (peek >= args.total_jobs ||
+                   peek / args.jobs_per_head != g / args.jobs_per_head) {
+              const int prev = atomicCAS(args.job_counter, peek, peek + 1);
+              if (prev == peek) {
+                job_slot[it_job & 1] = peek;
+                mode = 1;
+                break;
+              }
+              peek = prev;
+            }
+          }
+          // decision for job number it_job (the CTA's next job), slot (it_job - 1) % 2
+          claim_mode[(it_job - 1) & 1] = mode;
+          ptx::mbar_arrive(&bars[B_PF0 + ((it_job - 1) & 1)]);
+          if (mode == 1) ptx::mbar_arrive(&bars[B_JOB0 + (it_job & 1)]);
+        }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
@@ -334,6 +401,7 @@ __global__ void __launch_bounds__(512, 1)
       while (true) {
         ptx::mbar_wait_u(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
         const int g = __shfl_sync(0xffffffffu, job_slot[it_job & 1], 0);
+        if (lane == 0) slot_read(it_job);
         ++it_job;
         if (g >= args.total_jobs || __shfl_sync(0xffffffffu, ptx::aborted(), 0)) break;
         const JobView jv = decode_job(args, g);
@@ -416,6 +484,7 @@ __global__ void __launch_bounds__(512, 1)
       while (true) {
         ptx::mbar_wait(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
         const int g = job_slot[it_job & 1];
+        slot_read(it_job);
         if (g >= args.total_jobs) break;
         const JobView jv = decode_job(args, g);
         for (int t = jv.t0; t < jv.t1; ++t) {
@@ -435,8 +504,10 @@ __global__ void __launch_bounds__(512, 1)
               // every iteration); one acquire once the turn has come.
               if (ptx::ld_acquire(ticket) != rank_w) {
                 const long long t_start = clock64();
+                uint32_t polls = 0;
                 while (ptx::ld_relaxed(ticket) != rank_w) {
                   __nanosleep(32);
+                  if ((++polls & ptx::kAbortPollMask) != 0) continue;  // no extra round trip per poll
                   if (clock64() - t_start > 8 * ptx::kWatchdogCycles ||
                       *reinterpret_cast<volatile int*>(&ptx::g_dash_abort)) {  // ~35 s bound
                     atomicExch(args.error_flag, 1);
@@ -455,11 +526,12 @@ __global__ void __launch_bounds__(512, 1)
             const int grow = (par * args.B * args.H + jv.bh) * args.N + urow;
             const uint8_t* stg = smem + C::OFF_DQ + (x % NSTG) * C::DQ_BYTES;
             if constexpr (C::LINEAR) {
-              // two halves; the second may still be in the drain's hands
+              // NPART parts, each reduced as soon as the drain has written it;
+              // a part is handed back as soon as the bulk engine has read it
               float* dst0 = args.dqacc + static_cast<size_t>(grow) * D;
-              constexpr uint32_t HB = C::DQ_BYTES / 2;
+              constexpr uint32_t HB = C::DQ_BYTES / C::NPART;
 #pragma unroll
-              for (int hh = 0; hh < 2; ++hh) {
+              for (int hh = 0; hh < C::NPART; ++hh) {
                 if (!(args.debug & 4)) ptx::mbar_wait(&bars[B_AGF0 + hh * NAG + agent], ph);
                 if (!(args.debug & 1)) {
                   float* dst = dst0 + hh * (HB / 4);
@@ -467,12 +539,14 @@ __global__ void __launch_bounds__(512, 1)
                   else ptx::bulk_reduce_add_f32(dst, stg + hh * HB, HB);
                 }
                 ptx::bulk_commit();
+                if (hh >= 1) {
+                  ptx::bulk_wait_read<1>();  // part hh - 1 read: the drain may refill it
+                  ptx::mbar_arrive(part_empty(hh - 1));
+                }
               }
               if (h == 0) DASH_TRACE_MARK(8, x / C::NUNIT);
-              ptx::bulk_wait_read<1>();  // first half read: the drain may refill it
-              ptx::mbar_arrive(&bars[B_STG_EMPTY]);
               ptx::bulk_wait_read<0>();
-              ptx::mbar_arrive(&bars[B_STG_EMPTY1]);
+              ptx::mbar_arrive(part_empty(C::NPART - 1));
             } else {
               if (!(args.debug & 4)) ptx::mbar_wait(&bars[B_AGF0 + agent], ph);
 #pragma unroll
@@ -510,8 +584,13 @@ __global__ void __launch_bounds__(512, 1)
         ptx::mbar_arrive(&bars[B_JOB_DONE]);
         if (agent == 0) {
           ptx::mbar_wait(&bars[B_JOB_DONE], it_job & 1);
-          job_slot[(it_job + 1) & 1] = atomicAdd(args.job_counter, 1);
-          ptx::mbar_arrive(&bars[B_JOB0 + ((it_job + 1) & 1)]);
+          // did the producer already claim job it_job + 1?  (slot it_job % 2)
+          ptx::mbar_wait(&bars[B_PF0 + (it_job & 1)], (it_job >> 1) & 1);
+          if (claim_mode[it_job & 1] == 2) {
+            wait_slot_free(it_job + 1);
+            job_slot[(it_job + 1) & 1] = atomicAdd(args.job_counter, 1);
+            ptx::mbar_arrive(&bars[B_JOB0 + ((it_job + 1) & 1)]);
+          }
         }
         ++it_job;
       }
@@ -528,6 +607,8 @@ __global__ void __launch_bounds__(512, 1)
     while (true) {
       ptx::mbar_wait(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
       const int g = job_slot[it_job & 1];
+      __syncwarp();
+      if (lane == 0) slot_read(it_job);
       ++it_job;
       if (g >= args.total_jobs) break;
       const JobView jv = decode_job(args, g);
@@ -645,6 +726,8 @@ __global__ void __launch_bounds__(512, 1)
     while (true) {
       ptx::mbar_wait(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
       const int g = job_slot[it_job & 1];
+      __syncwarp();
+      if (lane == 0) slot_read(it_job);
       ++it_job;
       if (g >= args.total_jobs) break;
       const JobView jv = decode_job(args, g);
@@ -679,11 +762,11 @@ __global__ void __launch_bounds__(512, 1)
           const uint32_t y = x * C::NUNIT + h;  // staging unit
           if (args.debug & 4) continue;  // timing experiment: no staging (pure compute pipeline)
           if constexpr (C::LINEAR) {
-            // row-major [STG_ROWS][128] fp32 in two halves; lane tl = d index, v[c] = Q row c
-            constexpr int HR = C::STG_ROWS / 2;
+            // row-major [STG_ROWS][128] fp32 in NPART parts; lane tl = d index, v[c] = Q row c
+            constexpr int HR = C::STG_ROWS / C::NPART;
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              if (y >= 1) ptx::mbar_wait(&bars[hh ? B_STG_EMPTY1 : B_STG_EMPTY], (y - 1) & 1);
+            for (int hh = 0; hh < C::NPART; ++hh) {
+              if (y >= 1) ptx::mbar_wait(part_empty(hh), (y - 1) & 1);
 #pragma unroll
               for (int c = hh * HR; c < (hh + 1) * HR; ++c)
                 reinterpret_cast<float*>(stg0)[c * 128 + tl] = v[h * C::STG_ROWS + c];

@@ -286,6 +286,22 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     a.dqacc = dqacc;
     a.n_tickets = static_cast<int>(w.n_tickets);
     a.dump = g_dump;
+    static const int no_prefetch = [] {
+      const char* e = std::getenv("DASH_NO_PREFETCH");  // experiments only
+      return e ? std::atoi(e) : 0;
+    }();
+    // Early claim of the next job (bwd.cuh, producer) -- measured per schedule
+    // (profiles/r01_experiments/prefetch_claim.txt): it pays where a claimed
+    // job never waits on a job still queued behind another CTA's tail --
+    // the atomic variant (no waits), DESCENDING (its waits sit at each job's
+    // first Q tile) and NAIVE with the full mask; it costs up to 2x where a
+    // delayed job stalls a chain of later ones -- SHIFT (a head's cyclic jobs
+    // must run together) and NAIVE causal (staircase of unequal jobs).
+    a.prefetch = (!no_prefetch && (!deterministic || schedule == kDescending ||
+                                   (schedule == kNaive && !causal)))
+                     ? 1
+                     : 0;
+    a.cyclic = (deterministic && schedule == kShift) ? 1 : 0;
     auto kern = dash_bwd_kernel<D, V>;
     static bool attr_set = false;
     if (!attr_set) {
@@ -435,11 +451,14 @@ DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const voi
   launch_bwd<DD, VV>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule, deterministic, \
                      workspace, st)
   if (s->head_dim == 128)
-    return var == 3   ? DASH_LAUNCH(128, 3)
+    return var == 4   ? DASH_LAUNCH(128, 4)
+           : var == 3 ? DASH_LAUNCH(128, 3)
            : var == 2 ? DASH_LAUNCH(128, 2)
            : var == 1 ? DASH_LAUNCH(128, 1)
                       : DASH_LAUNCH(128, 0);
-  return var == 2 ? DASH_LAUNCH(64, 2) : var == 1 ? DASH_LAUNCH(64, 1) : DASH_LAUNCH(64, 0);
+  return var == 2 ? DASH_LAUNCH(64, 2)
+         : var == 1 ? DASH_LAUNCH(64, 1)
+                    : DASH_LAUNCH(64, 0);
 #undef DASH_LAUNCH
 }
 

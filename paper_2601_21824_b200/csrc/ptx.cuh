@@ -61,9 +61,16 @@ __device__ int g_dash_abort;
 // clock64 (per-SM cycles, monotonic) rather than %globaltimer, which the
 // driver may re-synchronise (jump) while a kernel runs.
 constexpr long long kWatchdogCycles = 1ll << 33;  // ~4.4 s at 1.965 GHz
+// The abort flag is a system-scope global load (~700 cycles to L2 and back):
+// it is read only every kAbortPollMask + 1 failed try_waits, so a wait that
+// just misses its phase does not add a global round trip to the latency of
+// the hand-off it is waiting for.
+constexpr uint32_t kAbortPollMask = 15;
 __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
   const long long t0 = clock64();
+  uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
+    if ((++spins & kAbortPollMask) != 0) continue;
     if (*reinterpret_cast<volatile int*>(&g_dash_abort)) return;
     if (clock64() - t0 > kWatchdogCycles) {
       printf("dash watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n",
@@ -84,10 +91,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // watchdog), so it can never hang the GPU.
 __device__ __forceinline__ void mbar_wait_u(uint64_t* bar, uint32_t parity) {
   asm volatile(
-      "{\n\t.reg .pred P1;\n\t.reg .b32 ab;\n\t"
+      "{\n\t.reg .pred P1;\n\t.reg .b32 ab, cnt;\n\t"
+      "mov.u32 cnt, 0;\n\t"
       "DASH_WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@P1 bra DASH_DONE_%=;\n\t"
+      "add.u32 cnt, cnt, 1;\n\t"
+      "and.b32 ab, cnt, 15;\n\t"  // abort flag every 16 misses (kAbortPollMask)
+      "setp.ne.u32 P1, ab, 0;\n\t"
+      "@P1 bra DASH_WAIT_%=;\n\t"
       "ld.volatile.global.u32 ab, [%2];\n\t"
       "setp.ne.u32 P1, ab, 0;\n\t"
       "@P1 bra DASH_DONE_%=;\n\t"
