@@ -71,6 +71,12 @@ struct BwdArgs {
   // the next job must belong to another head).
   int prefetch;
   int cyclic;
+  // Head grouping: job g covers the same KV tile(s) of G = head_group
+  // consecutive (b, h) heads, bh = (g / jobs_per_head) * G + hoff, each head's
+  // tasks in its own schedule order (task.y = rank | hoff << 16).  Per-head Q
+  // orders and reduction ranks are unchanged, so results are bit-identical
+  // for every G; G only amortises the per-job claim / drain cost.
+  int head_group;
 };
 
 // Per-(CTA, sub-tile) clock64 stamps for pipeline analysis; a null trace
@@ -97,7 +103,11 @@ struct BwdArgs {
 //        one half while the bulk engine still reads the other;
 // V = 4: as V = 3 with a ring of four quarters (16 rows, 8 KB each): a
 //        quarter is refilled as soon as the bulk engine has read it, so
-//        staging the next partial overlaps reading the previous one.
+//        staging the next partial overlaps reading the previous one;
+// V = 5: as V = 3 with a ring of THREE half-unit slots (48 KB: 1.5 partials
+//        of staging capacity), paid for by a single dS^T smem buffer (the
+//        softmax then waits for dQ of the previous sub-tile before writing
+//        dS^T).
 template <int D, int V = 0>
 struct BwdCfg {
   static constexpr int NTHREADS = 512;
@@ -106,8 +116,9 @@ struct BwdCfg {
   static constexpr int NSUB = 128 / BR;             // sub-tiles per schedule Q tile
   static constexpr int NSTAGE = (D == 128 && V != 1) ? 3 : 2;  // Q/dO/L/D ring depth
   static constexpr int NSTG = (V == 1 || V == 2) ? 2 : 1;     // dQ staging buffers
-  static constexpr bool LINEAR = (V == 3 || V == 4) && D == 128;  // 1-D bulk reduce of a linear tile
-  static constexpr int NPART = (V == 4) ? 4 : 2;                // linear staging ring parts
+  static constexpr bool LINEAR = (V == 3 || V == 4 || V == 5) && D == 128;  // 1-D bulk reduce
+  static constexpr int NPART = (V == 4) ? 4 : 2;  // linear staging: parts per partial
+  static constexpr int RING = (V == 5) ? 3 : NPART;  // linear staging: part slots in the ring
   static constexpr int NSMX = 2;                    // softmax warpgroups (column halves)
   static constexpr int SMX_COLS = BR / NSMX;        // columns per softmax thread
   static constexpr uint32_t KV_BYTES = BC * D * 2;
@@ -124,14 +135,15 @@ struct BwdCfg {
   static constexpr uint32_t OFF_V = OFF_K + KV_BYTES;
   static constexpr uint32_t OFF_Q = OFF_V + KV_BYTES;            // NSTAGE stages
   static constexpr uint32_t OFF_DO = OFF_Q + NSTAGE * Q_BYTES;   // NSTAGE stages
-  static constexpr int NDS = 2;                                  // dS^T smem buffers
+  static constexpr int NDS = (V == 5 && D == 128) ? 1 : 2;       // dS^T smem buffers
   static constexpr int NPT = 1;                                  // P^T TMEM buffers
   // d = 128: dS^T also lives in TMEM so dK += dS^T Q runs as a TS MMA (A from
   // TMEM, full rate, no smem read); d = 64 has no TMEM room left for it.
   static constexpr bool DS_IN_TMEM = (D == 128);
   static constexpr uint32_t OFF_DS = OFF_DO + NSTAGE * Q_BYTES;  // NDS x dS^T bf16 SW128
   static constexpr uint32_t OFF_DQ = OFF_DS + NDS * P_BYTES;     // fp32 SW128 staging buffer
-  static constexpr uint32_t OFF_L = OFF_DQ + NSTG * DQ_BYTES;    // NSTAGE x BR floats
+  static constexpr uint32_t STG_BYTES = LINEAR ? RING * (DQ_BYTES / NPART) : NSTG * DQ_BYTES;
+  static constexpr uint32_t OFF_L = OFF_DQ + STG_BYTES;           // NSTAGE x BR floats
   static constexpr uint32_t OFF_DV = OFF_L + NSTAGE * BR * 4;    // NSTAGE x BR floats
   static constexpr uint32_t OFF_BAR = OFF_DV + NSTAGE * BR * 4;
   static constexpr int NBAR = 40;
@@ -204,19 +216,35 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
-// Job decode shared by every role.
+// Job / task decode shared by every role.
 struct JobView {
-  int bh, b, h, t0, t1;
+  int bh0, t0, t1;  // first (b, h) head of the job's group; task range
 };
 __device__ __forceinline__ JobView decode_job(const BwdArgs& a, int g) {
   JobView j;
-  j.bh = g / a.jobs_per_head;
+  j.bh0 = (g / a.jobs_per_head) * a.head_group;
   const int lj = g % a.jobs_per_head;
-  j.b = j.bh / a.H;
-  j.h = j.bh % a.H;
   j.t0 = a.job_begin[lj];
   j.t1 = a.job_begin[lj + 1];
   return j;
+}
+struct TaskView {
+  int kv, q, rank, bh, b, h;
+  int seg;  // KV segment key: (kv, head) -- K/V, dK/dV change with it
+};
+__device__ __forceinline__ int task_seg(int2 tk) {
+  return (tk.x & 0xFFFF) | (tk.y & static_cast<int>(0xFFFF0000u));
+}
+__device__ __forceinline__ TaskView decode_task(const BwdArgs& a, const JobView& jv, int2 tk) {
+  TaskView v;
+  v.kv = tk.x & 0xFFFF;
+  v.q = tk.x >> 16;
+  v.rank = tk.y & 0xFFFF;
+  v.bh = jv.bh0 + (static_cast<unsigned>(tk.y) >> 16);
+  v.b = v.bh / a.H;
+  v.h = v.bh % a.H;
+  v.seg = task_seg(tk);
+  return v;
 }
 
 template <int D, int V>
@@ -291,22 +319,22 @@ __global__ void __launch_bounds__(512, 1)
         ++it_job;
         if (g >= args.total_jobs || __shfl_sync(0xffffffffu, ptx::aborted(), 0)) break;
         const JobView jv = decode_job(args, g);
-        int prev_kv = -1;
+        int prev_seg = -1;
         for (int t = jv.t0; t < jv.t1; ++t) {
-          const int2 tk = args.tasks[t];
-          const int kv = tk.x & 0xFFFF, q = tk.x >> 16;
-          if (kv != prev_kv) {
+          const TaskView tv = decode_task(args, jv, args.tasks[t]);
+          const int kv = tv.kv, q = tv.q;
+          if (tv.seg != prev_seg) {
             if (kv_cnt > 0) ptx::mbar_wait_u(&bars[B_KV_EMPTY], (kv_cnt - 1) & 1);
             ptx::mbar_arrive_expect_tx_e(&bars[B_KV_FULL], 2 * C::KV_BYTES);
 #pragma unroll
             for (int blk = 0; blk < D / 64; ++blk) {
               ptx::tma_load_2d_e(smem + C::OFF_K + blk * C::BC * 128, &tm_k, &bars[B_KV_FULL],
-                               jv.h * D + blk * 64, jv.b * args.N + kv * 128);
+                               tv.h * D + blk * 64, tv.b * args.N + kv * 128);
               ptx::tma_load_2d_e(smem + C::OFF_V + blk * C::BC * 128, &tm_v, &bars[B_KV_FULL],
-                               jv.h * D + blk * 64, jv.b * args.N + kv * 128);
+                               tv.h * D + blk * 64, tv.b * args.N + kv * 128);
             }
             ++kv_cnt;
-            prev_kv = kv;
+            prev_seg = tv.seg;
           }
           for (int sub = 0; sub < NSUB; ++sub) {
             const int stage = q_cnt % NSTAGE;
@@ -319,11 +347,11 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
             for (int blk = 0; blk < D / 64; ++blk) {
               ptx::tma_load_2d_e(smem + C::OFF_Q + stage * C::Q_BYTES + blk * BR * 128, &tm_q, full,
-                               jv.h * D + blk * 64, jv.b * args.N + row0);
+                               tv.h * D + blk * 64, tv.b * args.N + row0);
               ptx::tma_load_2d_e(smem + C::OFF_DO + stage * C::Q_BYTES + blk * BR * 128, &tm_do,
-                               full, jv.h * D + blk * 64, jv.b * args.N + row0);
+                               full, tv.h * D + blk * 64, tv.b * args.N + row0);
             }
-            const size_t lo = static_cast<size_t>(jv.bh) * args.N + row0;
+            const size_t lo = static_cast<size_t>(tv.bh) * args.N + row0;
             ptx::bulk_load_e(sL + stage * BR, args.lse2 + lo, BR * 4, full);
             ptx::bulk_load_e(sDv + stage * BR, args.Dvec + lo, BR * 4, full);
             ++q_cnt;
@@ -408,9 +436,9 @@ __global__ void __launch_bounds__(512, 1)
         const int t1 = __shfl_sync(0xffffffffu, jv.t1, 0);
         int ts = __shfl_sync(0xffffffffu, jv.t0, 0);
         while (ts < t1) {
-          const int kv = args.tasks[ts].x & 0xFFFF;
+          const int seg = task_seg(args.tasks[ts]);
           int te = ts + 1;
-          while (te < t1 && (args.tasks[te].x & 0xFFFF) == kv) ++te;
+          while (te < t1 && task_seg(args.tasks[te]) == seg) ++te;
           te = __shfl_sync(0xffffffffu, te, 0);
           const uint32_t nsub = static_cast<uint32_t>(te - ts) * NSUB;
           ptx::mbar_wait_u(&bars[B_KV_FULL], kv_cnt & 1);
@@ -488,8 +516,8 @@ __global__ void __launch_bounds__(512, 1)
         if (g >= args.total_jobs) break;
         const JobView jv = decode_job(args, g);
         for (int t = jv.t0; t < jv.t1; ++t) {
-          const int2 tk = args.tasks[t];
-          const int q = tk.x >> 16, rank = tk.y;
+          const TaskView tv = decode_task(args, jv, args.tasks[t]);
+          const int q = tv.q, rank = tv.rank;
           for (int sub = 0; sub < NSUB; ++sub) {
            for (int h = 0; h < C::NUNIT; ++h, ++x) {  // x counts staging units here
             if ((x % NAG) != agent) continue;
@@ -497,7 +525,7 @@ __global__ void __launch_bounds__(512, 1)
             const int urow = q * 128 + sub * BR + h * C::STG_ROWS;  // first Q row of the unit
             const int par = rank % args.split, rank_w = rank / args.split;  // AMB-27
             int* ticket = args.tickets + static_cast<size_t>(par) * args.n_tickets +
-                          static_cast<size_t>(jv.bh) * n_units + urow / C::STG_ROWS;
+                          static_cast<size_t>(tv.bh) * n_units + urow / C::STG_ROWS;
             if (det) {
               // Wait until the global order grants this block its turn (Alg.1 line 33).
               // Spin with relaxed loads (an acquire per poll would invalidate L1
@@ -523,30 +551,34 @@ __global__ void __launch_bounds__(512, 1)
             if (h == 0) DASH_TRACE_MARK(7, x / C::NUNIT);
             // Add dQ_local to dQ (Alg.1 line 34); rank 0 stores (no zero-fill needed).
             // row of dQacc [W][B*H*N, D]
-            const int grow = (par * args.B * args.H + jv.bh) * args.N + urow;
+            const int grow = (par * args.B * args.H + tv.bh) * args.N + urow;
             const uint8_t* stg = smem + C::OFF_DQ + (x % NSTG) * C::DQ_BYTES;
             if constexpr (C::LINEAR) {
               // NPART parts, each reduced as soon as the drain has written it;
               // a part is handed back as soon as the bulk engine has read it
               float* dst0 = args.dqacc + static_cast<size_t>(grow) * D;
               constexpr uint32_t HB = C::DQ_BYTES / C::NPART;
+              (void)stg;
 #pragma unroll
               for (int hh = 0; hh < C::NPART; ++hh) {
+                const uint32_t slot = (x * C::NPART + hh) % C::RING;  // part slot in the ring
                 if (!(args.debug & 4)) ptx::mbar_wait(&bars[B_AGF0 + hh * NAG + agent], ph);
+                if (h == 0 && hh == C::NPART - 1) DASH_TRACE_MARK(13, x / C::NUNIT);  // all parts staged
                 if (!(args.debug & 1)) {
                   float* dst = dst0 + hh * (HB / 4);
-                  if (det && rank_w == 0) ptx::bulk_store(dst, stg + hh * HB, HB);
-                  else ptx::bulk_reduce_add_f32(dst, stg + hh * HB, HB);
+                  const uint8_t* src = smem + C::OFF_DQ + slot * HB;
+                  if (det && rank_w == 0) ptx::bulk_store(dst, src, HB);
+                  else ptx::bulk_reduce_add_f32(dst, src, HB);
                 }
                 ptx::bulk_commit();
                 if (hh >= 1) {
-                  ptx::bulk_wait_read<1>();  // part hh - 1 read: the drain may refill it
-                  ptx::mbar_arrive(part_empty(hh - 1));
+                  ptx::bulk_wait_read<1>();  // part hh - 1 read: the drain may refill its slot
+                  ptx::mbar_arrive(part_empty((x * C::NPART + hh - 1) % C::RING));
                 }
               }
               if (h == 0) DASH_TRACE_MARK(8, x / C::NUNIT);
               ptx::bulk_wait_read<0>();
-              ptx::mbar_arrive(part_empty(C::NPART - 1));
+              ptx::mbar_arrive(part_empty((x * C::NPART + C::NPART - 1) % C::RING));
             } else {
               if (!(args.debug & 4)) ptx::mbar_wait(&bars[B_AGF0 + agent], ph);
 #pragma unroll
@@ -613,8 +645,8 @@ __global__ void __launch_bounds__(512, 1)
       if (g >= args.total_jobs) break;
       const JobView jv = decode_job(args, g);
       for (int t = jv.t0; t < jv.t1; ++t) {
-        const int2 tk = args.tasks[t];
-        const int kv = tk.x & 0xFFFF, q = tk.x >> 16;
+        const TaskView tv = decode_task(args, jv, args.tasks[t]);
+        const int kv = tv.kv, q = tv.q;
         const bool diag = args.causal && (kv == q);
         for (int sub = 0; sub < NSUB; ++sub, ++x) {
           const uint32_t st = x % NSTAGE, sb = x % C::NDS, pb = x % C::NPT;
@@ -684,12 +716,12 @@ __global__ void __launch_bounds__(512, 1)
           if (row == 0 && wg == 0) DASH_TRACE_MARK(4, x);
         }
         // End of a KV segment: dK/dV epilogue (local reduction done).
-        const bool seg_end = (t + 1 == jv.t1) || ((args.tasks[t + 1].x & 0xFFFF) != kv);
+        const bool seg_end = (t + 1 == jv.t1) || (task_seg(args.tasks[t + 1]) != tv.seg);
         if (seg_end) {
           ptx::mbar_wait(&bars[B_ACC_FULL], acc_cnt & 1);
           ++acc_cnt;
           ptx::tc_fence_after();
-          const size_t grow = (static_cast<size_t>(jv.b) * args.N + kv * 128 + row) * args.H + jv.h;
+          const size_t grow = (static_cast<size_t>(tv.b) * args.N + kv * 128 + row) * args.H + tv.h;
           __nv_bfloat16* dvp = args.dv + grow * D;
           __nv_bfloat16* dkp = args.dk + grow * D;
 #pragma unroll 1
@@ -744,9 +776,9 @@ __global__ void __launch_bounds__(512, 1)
         ptx::mbar_arrive(&bars[B_DQ_EMPTY]);
         if (args.dump) {
           // verification: the partial of (KV tile kv, these Q rows) -> dump[bh][kv][row][:]
-          const int2 tk = args.tasks[jv.t0 + u / NSUB];
-          const int urow0 = (tk.x >> 16) * 128 + (u % NSUB) * BR;
-          float* dp = args.dump + ((static_cast<size_t>(jv.bh) * (args.N / 128) + (tk.x & 0xFFFF)) *
+          const TaskView tv = decode_task(args, jv, args.tasks[jv.t0 + u / NSUB]);
+          const int urow0 = tv.q * 128 + (u % NSUB) * BR;
+          float* dp = args.dump + ((static_cast<size_t>(tv.bh) * (args.N / 128) + tv.kv) *
                                        args.N + urow0) * D;
           if constexpr (D == 128) {  // lane tl = d index, v[c] = Q row c
 #pragma unroll
@@ -766,10 +798,12 @@ __global__ void __launch_bounds__(512, 1)
             constexpr int HR = C::STG_ROWS / C::NPART;
 #pragma unroll
             for (int hh = 0; hh < C::NPART; ++hh) {
-              if (y >= 1) ptx::mbar_wait(part_empty(hh), (y - 1) & 1);
+              const uint32_t k = y * C::NPART + hh, slot = k % C::RING;  // part slot in the ring
+              if (k >= C::RING) ptx::mbar_wait(part_empty(slot), ((k / C::RING) - 1) & 1);
+              float* dst = reinterpret_cast<float*>(stg0 + slot * (C::DQ_BYTES / C::NPART));
 #pragma unroll
               for (int c = hh * HR; c < (hh + 1) * HR; ++c)
-                reinterpret_cast<float*>(stg0)[c * 128 + tl] = v[h * C::STG_ROWS + c];
+                dst[(c - hh * HR) * 128 + tl] = v[h * C::STG_ROWS + c];
               ptx::fence_async_smem();
               ptx::mbar_arrive(&bars[B_AGF0 + hh * NAG + (y % NAG)]);
             }
@@ -804,6 +838,7 @@ __global__ void __launch_bounds__(512, 1)
           ptx::mbar_arrive(&bars[B_AGF0 + (y % NAG)]);
         }
         if (tl == 0) DASH_TRACE_MARK(6, x);
+        if (tl == 96) DASH_TRACE_MARK(14, x);  // last drain warp done staging
       }
     }
   }

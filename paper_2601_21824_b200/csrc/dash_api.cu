@@ -58,6 +58,24 @@ int acc_split_for(int n) {
 }
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Head grouping G (bwd.cuh BwdArgs::head_group): a job covers its KV tile(s)
+// in G consecutive (b, h) heads, paying the per-job claim / refill once per G
+// heads; the heads' own schedules are untouched, so G never changes a bit
+// (tests pass bit-exact under forced G = 2, 4).  Measured
+// (profiles/r01_experiments/head_group.txt): it speeds up NAIVE at short
+// sequences (+5-10 %) but not SHIFT or DESCENDING -- their per-job tail is
+// the ordered-reduction pipeline draining, which grouping does not shorten --
+// so the default is G = 1; DASH_HEAD_GROUP forces G (experiments).
+int head_group_for(const dash_shape* s) {
+  static const int forced = [] {
+    const char* e = std::getenv("DASH_HEAD_GROUP");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int bh = s->batch * s->heads;
+  if (forced >= 1 && forced <= 8 && bh % forced == 0) return forced;
+  return 1;
+}
+
 bool shape_ok(const dash_shape* s) {
   if (!s) return false;
   if (s->batch < 1 || s->heads < 1 || s->seqlen < 128 || s->seqlen % 128) return false;
@@ -144,17 +162,25 @@ struct DevTable {
   int2* tasks = nullptr;
   int jobs = 0;
 };
-const DevTable* device_table(int dev, const ScheduleTable* t) {
+// With head grouping G (BwdArgs::head_group) job lj lists the tasks of the
+// per-head job lj once per head of the group, head offset in task.y's high half.
+const DevTable* device_table(int dev, const ScheduleTable* t, int G) {
   static std::mutex mu;
-  static std::map<std::tuple<int, int, int, int>, DevTable> cache;
+  static std::map<std::tuple<int, int, int, int, int>, DevTable> cache;
   std::lock_guard<std::mutex> lock(mu);
-  auto key = std::make_tuple(dev, t->schedule, t->n, t->mask);
+  auto key = std::make_tuple(dev, t->schedule, t->n, t->mask, G);
   auto it = cache.find(key);
   if (it != cache.end()) return &it->second;
-  std::vector<int> jb(t->job_begin.begin(), t->job_begin.end());
-  std::vector<int2> tk(t->tasks.size());
-  for (size_t i = 0; i < t->tasks.size(); ++i)
-    tk[i] = make_int2(t->tasks[i].kv | (t->tasks[i].q << 16), t->tasks[i].rank);
+  std::vector<int> jb(1, 0);
+  std::vector<int2> tk;
+  tk.reserve(t->tasks.size() * G);
+  for (int lj = 0; lj < t->jobs; ++lj) {
+    for (int hoff = 0; hoff < G; ++hoff)
+      for (int i = t->job_begin[lj]; i < t->job_begin[lj + 1]; ++i)
+        tk.push_back(make_int2(t->tasks[i].kv | (t->tasks[i].q << 16),
+                               t->tasks[i].rank | (hoff << 16)));
+    jb.push_back(static_cast<int>(tk.size()));
+  }
   DevTable d;
   d.jobs = t->jobs;
   void* buf = nullptr;
@@ -214,7 +240,8 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return DASH_ERR_CUDA;
   const int sms = device_sms(dev);
-  const int total_jobs = tab->jobs * s->batch * s->heads;
+  const int G = head_group_for(s);
+  const int total_jobs = tab->jobs * (s->batch * s->heads / G);
   int grid = total_jobs < sms ? total_jobs : sms;
   static const int debug_bits = [] {
     const char* e = std::getenv("DASH_DEBUG");
@@ -222,7 +249,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
   }();
 
   if (schedule == kShift && tab->jobs > grid) return DASH_ERR_UNSUPPORTED;
-  const DevTable* dt = device_table(dev, tab);
+  const DevTable* dt = device_table(dev, tab, G);
   if (!dt) return DASH_ERR_CUDA;
 
   const WsLayout w = ws_layout(s);
@@ -291,17 +318,16 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
       return e ? std::atoi(e) : 0;
     }();
     // Early claim of the next job (bwd.cuh, producer) -- measured per schedule
-    // (profiles/r01_experiments/prefetch_claim.txt): it pays where a claimed
-    // job never waits on a job still queued behind another CTA's tail --
-    // the atomic variant (no waits), DESCENDING (its waits sit at each job's
-    // first Q tile) and NAIVE with the full mask; it costs up to 2x where a
-    // delayed job stalls a chain of later ones -- SHIFT (a head's cyclic jobs
-    // must run together) and NAIVE causal (staircase of unequal jobs).
-    a.prefetch = (!no_prefetch && (!deterministic || schedule == kDescending ||
-                                   (schedule == kNaive && !causal)))
-                     ? 1
-                     : 0;
+    // (profiles/r01_experiments/prefetch_claim.txt, bench r01f): it pays for
+    // the atomic variant (no waits) and for DESCENDING on long sequences
+    // (n >= 64 tiles, where its waits sit at each job's first Q tile and W = 4);
+    // it costs up to 2x where a claimed job, queued behind its CTA's reduction
+    // tail, stalls a chain of later jobs -- SHIFT (a head's cyclic jobs must
+    // run together), NAIVE causal (staircase) and DESCENDING with W = 2 at
+    // d = 64.  NAIVE keeps the claim-after-release of the FA3-style baseline.
+    a.prefetch = (!no_prefetch && (!deterministic || (schedule == kDescending && n >= 64))) ? 1 : 0;
     a.cyclic = (deterministic && schedule == kShift) ? 1 : 0;
+    a.head_group = G;
     auto kern = dash_bwd_kernel<D, V>;
     static bool attr_set = false;
     if (!attr_set) {
@@ -451,7 +477,8 @@ DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const voi
   launch_bwd<DD, VV>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule, deterministic, \
                      workspace, st)
   if (s->head_dim == 128)
-    return var == 4   ? DASH_LAUNCH(128, 4)
+    return var == 5   ? DASH_LAUNCH(128, 5)
+           : var == 4 ? DASH_LAUNCH(128, 4)
            : var == 3 ? DASH_LAUNCH(128, 3)
            : var == 2 ? DASH_LAUNCH(128, 2)
            : var == 1 ? DASH_LAUNCH(128, 1)

@@ -39,4 +39,4 @@ for N in seqlens:
             res.append(f"{sched}{'' if det else '-atomic'}={fl * 10 / (e0.elapsed_time(e1) / 1e3) / 1e12:.0f}")
         except dash.DashError as e:
             res.append(f"{sched}=ERR")
-    print(f"DEBUG={dbg} PF={0 if os.environ.get('DASH_NO_PREFETCH', '0') == '1' else 1} VAR={os.environ.get('DASH_VARIANT', '-')} W={dash.acc_split(N)} N={N} d={d} {'causal' if causal else 'full'}: " + " ".join(res), flush=True)
+    print(f"DEBUG={dbg} G={os.environ.get('DASH_HEAD_GROUP', '-')} PF={0 if os.environ.get('DASH_NO_PREFETCH', '0') == '1' else 1} VAR={os.environ.get('DASH_VARIANT', '-')} W={dash.acc_split(N)} N={N} d={d} {'causal' if causal else 'full'}: " + " ".join(res), flush=True)

@@ -29,7 +29,7 @@ def main():
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--atomic", action="store_true")
     ap.add_argument("--out", default=None)
-    ap.add_argument("--npz", default=None, help="also save the raw stamps [grid, sub-tiles, 13]")
+    ap.add_argument("--npz", default=None, help="also save the raw stamps [grid, sub-tiles, 16]")
     args = ap.parse_args()
     causal = not args.full
     B, N, H, d = sweep_shape(args.seqlen, args.head_dim)
@@ -44,7 +44,7 @@ def main():
     t = tr.cpu().numpy().astype(np.int64)  # [grid, cap, 16]
     if args.npz:
         nmax = int(max(np.count_nonzero(t[c, :, 0]) for c in range(t.shape[0])))
-        np.savez_compressed(args.npz, stamps=t[:, :nmax, :13])
+        np.savez_compressed(args.npz, stamps=t[:, :nmax, :16])
     res = {"seqlen": N, "head_dim": d, "schedule": args.schedule, "causal": causal,
            "deterministic": not args.atomic}
     per = {}
