@@ -107,7 +107,15 @@ struct BwdArgs {
 // V = 5: as V = 3 with a ring of THREE half-unit slots (48 KB: 1.5 partials
 //        of staging capacity), paid for by a single dS^T smem buffer (the
 //        softmax then waits for dQ of the previous sub-tile before writing
-//        dS^T).
+//        dS^T);
+// V = 6: split reduction (d = 128): rows 0-31 of a partial are staged and
+//        reduced by the bulk engine (1-D, ring of two 16 KB slots), rows 32-63
+//        are added by the drain warps straight from registers with
+//        red.global.add.f32 (st.global for the first contribution) once the
+//        agent has acquired the ticket -- the two halves travel to L2 in
+//        parallel.  The agent releases the ticket after its bulk writes have
+//        completed and every drain thread has arrived (release.cta) after its
+//        red ops, so the ticket's st.release.gpu is cumulative over both.
 template <int D, int V = 0>
 struct BwdCfg {
   static constexpr int NTHREADS = 512;
@@ -117,6 +125,7 @@ struct BwdCfg {
   static constexpr int NSTAGE = (D == 128 && V != 1) ? 3 : 2;  // Q/dO/L/D ring depth
   static constexpr int NSTG = (V == 1 || V == 2) ? 2 : 1;     // dQ staging buffers
   static constexpr bool LINEAR = (V == 3 || V == 4 || V == 5) && D == 128;  // 1-D bulk reduce
+  static constexpr bool SPLITRED = (V == 6 && D == 128);  // half bulk, half red.global
   static constexpr int NPART = (V == 4) ? 4 : 2;  // linear staging: parts per partial
   static constexpr int RING = (V == 5) ? 3 : NPART;  // linear staging: part slots in the ring
   static constexpr int NSMX = 2;                    // softmax warpgroups (column halves)
@@ -142,7 +151,8 @@ struct BwdCfg {
   static constexpr bool DS_IN_TMEM = (D == 128);
   static constexpr uint32_t OFF_DS = OFF_DO + NSTAGE * Q_BYTES;  // NDS x dS^T bf16 SW128
   static constexpr uint32_t OFF_DQ = OFF_DS + NDS * P_BYTES;     // fp32 SW128 staging buffer
-  static constexpr uint32_t STG_BYTES = LINEAR ? RING * (DQ_BYTES / NPART) : NSTG * DQ_BYTES;
+  static constexpr uint32_t STG_BYTES =
+      LINEAR ? RING * (DQ_BYTES / NPART) : SPLITRED ? DQ_BYTES : NSTG * DQ_BYTES;
   static constexpr uint32_t OFF_L = OFF_DQ + STG_BYTES;           // NSTAGE x BR floats
   static constexpr uint32_t OFF_DV = OFF_L + NSTAGE * BR * 4;    // NSTAGE x BR floats
   static constexpr uint32_t OFF_BAR = OFF_DV + NSTAGE * BR * 4;
@@ -185,6 +195,8 @@ enum : int {
   B_STG_EMPTY2 = 16, B_STG_EMPTY3 = 17, // linear staging parts 2, 3 read (1), V = 4
   B_PF0 = 24,                          // + (t - 1) % 2: producer's claim decision for job t (1)
   B_SLOT_FREE0 = 30,                   // + j % 2: every warp has read job j's slot (16)
+  B_TKT0 = 36,                         // + agent: ticket of the agent's unit acquired (1), V = 6
+  B_RDONE0 = 38,                       // + agent: drain's direct half added (128), V = 6
   B_AGF0 = 32,                         // + h * NAG + agent: staging (part h) written for
                                        // the agent of unit x (x % NAG) (128)
   B_COUNT = 40
@@ -291,6 +303,8 @@ __global__ void __launch_bounds__(512, 1)
     for (int i = 0; i < C::NPART * NAG; ++i) ptx::mbar_init(&bars[B_AGF0 + i], 128);
     ptx::mbar_init(&bars[B_JOB_DONE], NAG);
     ptx::mbar_init(&bars[B_SLOT_FREE0], 16);
+    if constexpr (C::SPLITRED)
+      for (int i = 0; i < NAG; ++i) ptx::mbar_init(&bars[B_RDONE0 + i], 128);
     ptx::mbar_init(&bars[B_SLOT_FREE0 + 1], 16);
     ptx::fence_mbar_init();
     ptx::fence_async_smem();
@@ -553,7 +567,25 @@ __global__ void __launch_bounds__(512, 1)
             // row of dQacc [W][B*H*N, D]
             const int grow = (par * args.B * args.H + tv.bh) * args.N + urow;
             const uint8_t* stg = smem + C::OFF_DQ + (x % NSTG) * C::DQ_BYTES;
-            if constexpr (C::LINEAR) {
+            if constexpr (C::SPLITRED) {
+              // the drain may now add rows 32-63 itself (ordered after this acquire)
+              ptx::mbar_arrive(&bars[B_TKT0 + agent]);
+              constexpr uint32_t HB = C::DQ_BYTES / 2;
+              const uint32_t slot = x & 1;
+              ptx::mbar_wait(&bars[B_AGF0 + agent], ph);
+              if (h == 0) DASH_TRACE_MARK(13, x / C::NUNIT);
+              float* dst = args.dqacc + static_cast<size_t>(grow) * D;
+              const uint8_t* src = smem + C::OFF_DQ + slot * HB;
+              if (det && rank_w == 0) ptx::bulk_store(dst, src, HB);
+              else ptx::bulk_reduce_add_f32(dst, src, HB);
+              ptx::bulk_commit();
+              if (h == 0) DASH_TRACE_MARK(8, x / C::NUNIT);
+              ptx::bulk_wait_read<0>();
+              ptx::mbar_arrive(part_empty(slot));
+              // completion of both halves before the release: own bulk writes
+              // (wait_group below) and the drain's red ops (its arrive, release.cta)
+              ptx::mbar_wait(&bars[B_RDONE0 + agent], ph);
+            } else if constexpr (C::LINEAR) {
               // NPART parts, each reduced as soon as the drain has written it;
               // a part is handed back as soon as the bulk engine has read it
               float* dst0 = args.dqacc + static_cast<size_t>(grow) * D;
@@ -793,6 +825,36 @@ __global__ void __launch_bounds__(512, 1)
         for (int h = 0; h < C::NUNIT; ++h) {
           const uint32_t y = x * C::NUNIT + h;  // staging unit
           if (args.debug & 4) continue;  // timing experiment: no staging (pure compute pipeline)
+          if constexpr (C::SPLITRED) {
+            // rows 0-31 -> bulk-engine staging slot y % 2; lane tl = d index, v[c] = Q row c
+            constexpr int HR = BR / 2;
+            const uint32_t slot = y & 1;
+            if (y >= 2) ptx::mbar_wait(part_empty(slot), ((y >> 1) - 1) & 1);
+            float* sdst = reinterpret_cast<float*>(stg0 + slot * (C::DQ_BYTES / 2));
+#pragma unroll
+            for (int c = 0; c < HR; ++c) sdst[c * 128 + tl] = v[c];
+            ptx::fence_async_smem();
+            ptx::mbar_arrive(&bars[B_AGF0 + (y % NAG)]);
+            if (tl == 0) DASH_TRACE_MARK(6, x);
+            // rows 32-63 straight to dQacc once the unit's ticket is held
+            const TaskView tv = decode_task(args, jv, args.tasks[jv.t0 + u / NSUB]);
+            const int rank = tv.rank, par = rank % args.split;
+            const bool first = args.deterministic && rank / args.split == 0;
+            const size_t grow = static_cast<size_t>(par * args.B * args.H + tv.bh) * args.N +
+                                tv.q * 128 + (u % NSUB) * BR + HR;
+            float* gdst = args.dqacc + grow * D + tl;
+            ptx::mbar_wait(&bars[B_TKT0 + (y % NAG)], (y / NAG) & 1);
+            if (first) {
+#pragma unroll
+              for (int c = HR; c < BR; ++c) gdst[(c - HR) * D] = v[c];
+            } else {
+#pragma unroll
+              for (int c = HR; c < BR; ++c) ptx::red_add_f32(gdst + (c - HR) * D, v[c]);
+            }
+            ptx::mbar_arrive(&bars[B_RDONE0 + (y % NAG)]);
+            if (tl == 96) DASH_TRACE_MARK(14, x);
+            continue;
+          }
           if constexpr (C::LINEAR) {
             // row-major [STG_ROWS][128] fp32 in NPART parts; lane tl = d index, v[c] = Q row c
             constexpr int HR = C::STG_ROWS / C::NPART;

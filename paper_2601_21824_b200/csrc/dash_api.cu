@@ -477,7 +477,8 @@ DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const voi
   launch_bwd<DD, VV>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule, deterministic, \
                      workspace, st)
   if (s->head_dim == 128)
-    return var == 5   ? DASH_LAUNCH(128, 5)
+    return var == 6   ? DASH_LAUNCH(128, 6)
+           : var == 5 ? DASH_LAUNCH(128, 5)
            : var == 4 ? DASH_LAUNCH(128, 4)
            : var == 3 ? DASH_LAUNCH(128, 3)
            : var == 2 ? DASH_LAUNCH(128, 2)

@@ -1,0 +1,83 @@
+"""Runtime choices never change bits (DESIGN.md AMB-22, AMB-27, AMB-28).
+
+The library takes several decisions that are not part of the method: the
+staging variant of the ordered reduction (DASH_VARIANT), early claiming of
+the next job (on for DESCENDING at n >= 64 and the atomic variant; off with
+DASH_NO_PREFETCH=1) and head grouping (DASH_HEAD_GROUP=G: one job covers G
+heads).  None of them may change any head's Q order or reduction ranks, so
+the deterministic dq/dk/dv must be bit-identical under every setting.  The
+settings are read once per process, so each runs in a subprocess that prints
+SHA-256 digests of the outputs; the digests must all equal the default run's.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# (B, N, H, d, causal, schedule): N = 8192 makes DESCENDING claim early (n = 64)
+CASES = [
+    (2, 1024, 4, 128, True, "shift"),
+    (2, 1024, 4, 128, False, "shift"),
+    (2, 1024, 4, 64, True, "naive"),
+    (1, 8192, 2, 128, True, "descending"),
+    (1, 1024, 4, 64, False, "descending"),
+]
+
+SCRIPT = r"""
+import hashlib, json, sys
+sys.path.insert(0, sys.argv[1])
+import torch
+from paper_2601_21824_b200 import dash
+from paper_2601_21824_b200.inputs import attn_inputs
+cases = json.loads(sys.argv[2])
+out = []
+for B, N, H, d, causal, sched in cases:
+    g = {k: v.cuda() for k, v in attn_inputs(B, N, H, d, seed=11).items()}
+    o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], causal)
+    res = dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal, sched, True)
+    torch.cuda.synchronize()
+    out.append([hashlib.sha256(t.cpu().view(torch.int16).numpy().tobytes()).hexdigest()
+                for t in res])
+print(json.dumps(out))
+"""
+
+
+def _digests(env_extra):
+    env = dict(os.environ)
+    for k in ("DASH_VARIANT", "DASH_NO_PREFETCH", "DASH_HEAD_GROUP"):
+        env.pop(k, None)
+    env.update(env_extra)
+    r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, json.dumps(CASES)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+@pytest.fixture(scope="module")
+def reference_digests():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2601_21824_b200 import build
+    build.build()
+    return _digests({})
+
+
+@pytest.mark.parametrize("env", [
+    {"DASH_NO_PREFETCH": "1"},
+    {"DASH_HEAD_GROUP": "2"},
+    {"DASH_HEAD_GROUP": "4"},
+    {"DASH_VARIANT": "0"},
+    {"DASH_VARIANT": "5"},
+    {"DASH_VARIANT": "6"},
+], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_runtime_choice_keeps_bits(reference_digests, env):
+    got = _digests(env)
+    for case, a, b in zip(CASES, got, reference_digests):
+        assert a == b, f"{env} changed the bits of {case}"
