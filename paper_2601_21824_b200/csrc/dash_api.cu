@@ -319,13 +319,15 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     }();
     // Early claim of the next job (bwd.cuh, producer) -- measured per schedule
     // (profiles/r01_experiments/prefetch_claim.txt, bench r01f): it pays for
-    // the atomic variant (no waits) and for DESCENDING on long sequences
-    // (n >= 64 tiles, where its waits sit at each job's first Q tile and W = 4);
+    // the atomic variant (no waits) and for DESCENDING with W = 4 interleaved
+    // accumulators (automatic at n >= 64; its waits sit at each job's first Q
+    // tile); with W = 1 (config-5 model check) it is slower;
     // it costs up to 2x where a claimed job, queued behind its CTA's reduction
     // tail, stalls a chain of later jobs -- SHIFT (a head's cyclic jobs must
     // run together), NAIVE causal (staircase) and DESCENDING with W = 2 at
     // d = 64.  NAIVE keeps the claim-after-release of the FA3-style baseline.
-    a.prefetch = (!no_prefetch && (!deterministic || (schedule == kDescending && n >= 64))) ? 1 : 0;
+    a.prefetch =
+        (!no_prefetch && (!deterministic || (schedule == kDescending && a.split >= 4))) ? 1 : 0;
     a.cyclic = (deterministic && schedule == kShift) ? 1 : 0;
     a.head_group = G;
     auto kern = dash_bwd_kernel<D, V>;
