@@ -115,10 +115,18 @@ dash_status dash_attn_bwd(const dash_shape* shape, const void* q, const void* k,
                           void* stream);
 
 /* End-to-end variant with HOST buffers: q, k, v, o, dout, lse are host
- * pointers (pinned memory recommended), dq, dk, dv host outputs.  Copies the
- * inputs into `workspace` (device), runs dash_attn_bwd, copies the results
- * back and synchronises `stream` before returning.  Workspace size:
- * dash_attn_bwd_host_workspace_bytes(). */
+ * pointers (pinned memory recommended: pageable memory makes the copies
+ * synchronous), dq, dk, dv host outputs, same layouts as dash_attn_bwd.
+ * The (b, h) heads are split into chunks (batch ranges, or head ranges of one
+ * batch when B is small) that stream through three device slots of
+ * `workspace` on three library-owned streams: the H2D copy of chunk i+1, the
+ * backward of chunk i and the D2H copy of chunk i-1 overlap.  A chunk is a
+ * (b, h) shard, so the results are bit-identical to dash_attn_bwd on the
+ * whole problem.  Work queued on `stream` before the call is waited for; the
+ * call returns after the last copy has completed and `stream` is ordered
+ * after it.  Workspace size: dash_attn_bwd_host_workspace_bytes() (three
+ * chunk slots, each with its own dash_attn_bwd workspace).  Errors as
+ * dash_attn_bwd; DASH_ERR_INVALID_ARG also for a null host pointer. */
 size_t dash_attn_bwd_host_workspace_bytes(const dash_shape* shape, int causal, int schedule,
                                           int deterministic);
 dash_status dash_attn_bwd_host(const dash_shape* shape, const void* q, const void* k,

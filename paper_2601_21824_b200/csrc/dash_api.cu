@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -545,13 +546,46 @@ DASH_API dash_status dash_attn_bwd_dump(const dash_shape* s, const void* q, cons
 }
 
 namespace {
-struct HostWs {
-  size_t in_bytes, lse_bytes, q, k, v, o, dout, lse, dq, dk, dv, inner, total;
+// End-to-end path (dash_attn_bwd_host): the (b, h) heads are split into
+// chunks -- batch ranges, or head ranges of one batch when B < 4 -- and the
+// chunks stream through three device slots on three library streams:
+// H2D of chunk i+1 || backward of chunk i || D2H of chunk i-1.  A chunk is a
+// (b, h) shard, so its results are bit-identical to the one-shot call
+// (tests/test_gpu_bwd.py::test_host_path_matches_device_path).
+constexpr int kHostSlots = 3;
+// target number of chunks per call (DASH_HOST_CHUNKS overrides; experiments)
+int host_chunks() {
+  static const int c = [] {
+    const char* e = std::getenv("DASH_HOST_CHUNKS");
+    const int v = e ? std::atoi(e) : 0;
+    return v >= 1 ? v : 8;
+  }();
+  return c;
+}
+struct HostPlan {
+  int nb, nh;          // chunk shape: nb batches x nh heads (nb == B or nh == H)
+  int chunks_b, chunks_h;
+  size_t in_bytes, lse_bytes;  // per chunk (largest)
+  size_t q, k, v, o, dout, lse, dq, dk, dv, inner, slot, total;
 };
-HostWs host_ws(const dash_shape* s) {
-  HostWs h;
-  h.in_bytes = static_cast<size_t>(s->batch) * s->seqlen * s->heads * s->head_dim * 2;
-  h.lse_bytes = static_cast<size_t>(s->batch) * s->heads * s->seqlen * 4;
+HostPlan host_plan(const dash_shape* s) {
+  HostPlan h;
+  const int kc = host_chunks();
+  if (s->batch >= kc) {
+    h.nb = (s->batch + kc - 1) / kc;
+    h.nh = s->heads;
+  } else {
+    const int hb = (kc + s->batch - 1) / s->batch;  // head blocks per batch
+    h.nb = 1;
+    h.nh = (s->heads + hb - 1) / hb;
+  }
+  h.chunks_b = (s->batch + h.nb - 1) / h.nb;
+  h.chunks_h = (s->heads + h.nh - 1) / h.nh;
+  dash_shape cs = *s;
+  cs.batch = h.nb;
+  cs.heads = h.nh;
+  h.in_bytes = static_cast<size_t>(h.nb) * s->seqlen * h.nh * s->head_dim * 2;
+  h.lse_bytes = static_cast<size_t>(h.nb) * h.nh * s->seqlen * 4;
   size_t off = 0;
   size_t* slots[] = {&h.q, &h.k, &h.v, &h.o, &h.dout, &h.dq, &h.dk, &h.dv};
   for (size_t* sl : slots) {
@@ -561,8 +595,52 @@ HostWs host_ws(const dash_shape* s) {
   h.lse = off;
   off = align_up(off + h.lse_bytes, kAlign);
   h.inner = off;
-  h.total = off + ws_layout(s).total;
+  h.slot = align_up(off + ws_layout(&cs).total, kAlign);
+  h.total = kHostSlots * h.slot;
   return h;
+}
+struct HostStreams {
+  cudaStream_t h2d, comp, d2h;
+  cudaEvent_t start, in_done[kHostSlots], comp_done[kHostSlots], out_done[kHostSlots];
+};
+const HostStreams* host_streams(int dev) {
+  static std::mutex mu;
+  static std::map<int, HostStreams> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return &it->second;
+  HostStreams hs;
+  cudaStreamCreateWithFlags(&hs.h2d, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&hs.comp, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&hs.d2h, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&hs.start, cudaEventDisableTiming);
+  for (int i = 0; i < kHostSlots; ++i) {
+    cudaEventCreateWithFlags(&hs.in_done[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&hs.comp_done[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&hs.out_done[i], cudaEventDisableTiming);
+  }
+  cache[dev] = hs;
+  return &cache[dev];
+}
+// Copies the chunk (b0.., h0..) of a [B,N,H,d] bf16 tensor between host and a
+// packed [nb,N,nh,d] device buffer (2-D copy when the chunk is a head range).
+cudaError_t copy_chunk(void* dst, const void* src, const dash_shape* s, int b0, int nb, int h0,
+                       int nh, bool to_device, cudaStream_t st) {
+  const size_t row = static_cast<size_t>(s->head_dim) * 2;
+  if (nh == s->heads) {
+    const size_t off = static_cast<size_t>(b0) * s->seqlen * s->heads * row;
+    const size_t bytes = static_cast<size_t>(nb) * s->seqlen * s->heads * row;
+    return to_device ? cudaMemcpyAsync(dst, static_cast<const char*>(src) + off, bytes,
+                                       cudaMemcpyHostToDevice, st)
+                     : cudaMemcpyAsync(static_cast<char*>(dst) + off, src, bytes,
+                                       cudaMemcpyDeviceToHost, st);
+  }
+  const size_t hoff = (static_cast<size_t>(b0) * s->seqlen * s->heads + h0) * row;
+  const size_t hpitch = s->heads * row, dpitch = nh * row;
+  return to_device ? cudaMemcpy2DAsync(dst, dpitch, static_cast<const char*>(src) + hoff, hpitch,
+                                       dpitch, s->seqlen, cudaMemcpyHostToDevice, st)
+                   : cudaMemcpy2DAsync(static_cast<char*>(dst) + hoff, hpitch, src, dpitch, dpitch,
+                                       s->seqlen, cudaMemcpyDeviceToHost, st);
 }
 }  // namespace
 
@@ -572,7 +650,7 @@ DASH_API size_t dash_attn_bwd_host_workspace_bytes(const dash_shape* s, int caus
   (void)schedule;
   (void)deterministic;
   if (!shape_ok(s)) return 0;
-  return host_ws(s).total;
+  return host_plan(s).total;
 }
 
 DASH_API dash_status dash_attn_bwd_host(const dash_shape* s, const void* q, const void* k,
@@ -585,26 +663,64 @@ DASH_API dash_status dash_attn_bwd_host(const dash_shape* s, const void* q, cons
   for (const void* p : hptrs)
     if (!p) return DASH_ERR_INVALID_ARG;
   if (!aligned16(workspace)) return DASH_ERR_INVALID_ARG;
-  const HostWs h = host_ws(s);
+  const HostPlan h = host_plan(s);
   if (workspace_bytes < h.total) return DASH_ERR_WORKSPACE;
-  char* w = static_cast<char*>(workspace);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return DASH_ERR_CUDA;
+  const HostStreams* hs = host_streams(dev);
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const std::pair<size_t, const void*> ins[] = {{h.q, q}, {h.k, k}, {h.v, v}, {h.o, o}, {h.dout, dout}};
-  for (auto& in : ins)
-    if (cudaMemcpyAsync(w + in.first, in.second, h.in_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
-      return DASH_ERR_CUDA;
-  if (cudaMemcpyAsync(w + h.lse, lse, h.lse_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
-    return DASH_ERR_CUDA;
-  dash_status r = dash_attn_bwd(s, w + h.q, w + h.k, w + h.v, w + h.o, w + h.dout,
-                                reinterpret_cast<const float*>(w + h.lse), w + h.dq, w + h.dk,
-                                w + h.dv, causal, schedule, deterministic, w + h.inner,
-                                h.total - h.inner, stream);
-  if (r != DASH_OK) return r;
-  const std::pair<void*, size_t> outs[] = {{dq, h.dq}, {dk, h.dk}, {dv, h.dv}};
-  for (auto& out : outs)
-    if (cudaMemcpyAsync(out.first, w + out.second, h.in_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
-      return DASH_ERR_CUDA;
-  return cudaStreamSynchronize(st) == cudaSuccess ? DASH_OK : DASH_ERR_CUDA;
+  // respect work already queued on the caller's stream
+  if (cudaEventRecord(hs->start, st) != cudaSuccess) return DASH_ERR_CUDA;
+  cudaStreamWaitEvent(hs->h2d, hs->start, 0);
+  char* base = static_cast<char*>(workspace);
+  int idx = 0;
+  for (int cb = 0; cb < h.chunks_b; ++cb) {
+    for (int ch = 0; ch < h.chunks_h; ++ch, ++idx) {
+      const int b0 = cb * h.nb, nb = std::min(h.nb, s->batch - b0);
+      const int h0 = ch * h.nh, nh = std::min(h.nh, s->heads - h0);
+      const int slot = idx % kHostSlots;
+      char* w = base + static_cast<size_t>(slot) * h.slot;
+      // H2D (slot free once chunk idx - kHostSlots has been copied out)
+      if (idx >= kHostSlots) cudaStreamWaitEvent(hs->h2d, hs->out_done[slot], 0);
+      const void* ins[] = {q, k, v, o, dout};
+      const size_t ioff[] = {h.q, h.k, h.v, h.o, h.dout};
+      for (int t = 0; t < 5; ++t)
+        if (copy_chunk(w + ioff[t], ins[t], s, b0, nb, h0, nh, true, hs->h2d) != cudaSuccess)
+          return DASH_ERR_CUDA;
+      const size_t loff = (static_cast<size_t>(b0) * s->heads + h0) * s->seqlen * 4;
+      if (cudaMemcpy2DAsync(w + h.lse, static_cast<size_t>(nh) * s->seqlen * 4,
+                            reinterpret_cast<const char*>(lse) + loff,
+                            static_cast<size_t>(s->heads) * s->seqlen * 4,
+                            static_cast<size_t>(nh) * s->seqlen * 4, nb, cudaMemcpyHostToDevice,
+                            hs->h2d) != cudaSuccess)
+        return DASH_ERR_CUDA;
+      cudaEventRecord(hs->in_done[slot], hs->h2d);
+      // backward of the chunk (a (b, h) shard: same bits as the full call)
+      cudaStreamWaitEvent(hs->comp, hs->in_done[slot], 0);
+      dash_shape cs = *s;
+      cs.batch = nb;
+      cs.heads = nh;
+      const dash_status r =
+          dash_attn_bwd(&cs, w + h.q, w + h.k, w + h.v, w + h.o, w + h.dout,
+                        reinterpret_cast<const float*>(w + h.lse), w + h.dq, w + h.dk, w + h.dv,
+                        causal, schedule, deterministic, w + h.inner, h.slot - h.inner, hs->comp);
+      if (r != DASH_OK) return r;
+      cudaEventRecord(hs->comp_done[slot], hs->comp);
+      // D2H
+      cudaStreamWaitEvent(hs->d2h, hs->comp_done[slot], 0);
+      void* outs[] = {dq, dk, dv};
+      const size_t ooff[] = {h.dq, h.dk, h.dv};
+      for (int t = 0; t < 3; ++t)
+        if (copy_chunk(outs[t], w + ooff[t], s, b0, nb, h0, nh, false, hs->d2h) != cudaSuccess)
+          return DASH_ERR_CUDA;
+      cudaEventRecord(hs->out_done[slot], hs->d2h);
+    }
+  }
+  cudaEventRecord(hs->start, hs->d2h);
+  cudaStreamWaitEvent(st, hs->start, 0);
+  return cudaStreamSynchronize(hs->d2h) == cudaSuccess && cudaGetLastError() == cudaSuccess
+             ? DASH_OK
+             : DASH_ERR_CUDA;
 }
 
 DASH_API dash_status dash_check_workspace(const dash_shape* s, int causal, int schedule,

@@ -223,3 +223,28 @@ def test_auto_schedule_runs_the_resolved_schedule(dash, N, causal):
     _, _, *b = _run(dash, g, causal, want, True)
     for x, y in zip(a, b):
         assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("B,N,H,d,causal,schedule", [
+    (5, 512, 3, 128, True, "shift"),     # batch-range chunks, uneven last chunk
+    (1, 1024, 6, 64, False, "shift"),    # head-range chunks (2-D copies), B < 4
+    (2, 512, 5, 128, True, "descending"),  # head ranges of 3 + 2 heads per batch
+])
+def test_host_path_matches_device_path(dash, B, N, H, d, causal, schedule):
+    """dash_attn_bwd_host streams (b, h) chunks through three device slots
+    (H2D || backward || D2H); chunks are (b, h) shards, so the host-buffer
+    results must equal the device call bit for bit."""
+    cpu, g = _inputs(B, N, H, d, seed=9)
+    o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], causal)
+    ref = dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal, schedule, True)
+    torch.cuda.synchronize()
+    hb = {"q": cpu["q"], "k": cpu["k"], "v": cpu["v"], "o": o.cpu(), "do": cpu["do"],
+          "lse": lse.cpu()}
+    hb = {k: v.contiguous().pin_memory() for k, v in hb.items()}
+    outs = [torch.empty_like(hb["q"]).pin_memory() for _ in range(3)]
+    ws = torch.empty(dash.host_workspace_bytes((B, N, H, d), causal), dtype=torch.uint8,
+                     device="cuda")
+    dash.attn_bwd_host(hb["q"], hb["k"], hb["v"], hb["o"], hb["do"], hb["lse"], *outs, causal,
+                       schedule, True, ws)
+    for a, r in zip(outs, ref):
+        assert torch.equal(a, r.cpu())
