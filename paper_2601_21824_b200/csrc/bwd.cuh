@@ -31,6 +31,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <type_traits>
+
 #include "umma.cuh"
 
 namespace dash {
@@ -676,8 +678,13 @@ __global__ void __launch_bounds__(512, 1)
       ++it_job;
       if (g >= args.total_jobs) break;
       const JobView jv = decode_job(args, g);
+      // The next task's entry is loaded one task ahead: its L2 latency (~700
+      // cycles) otherwise sits between two sub-tiles on the softmax's
+      // critical path (every sub-tile at d = 64, where a task is one sub-tile).
+      int2 tk_cur = args.tasks[jv.t0];
       for (int t = jv.t0; t < jv.t1; ++t) {
-        const TaskView tv = decode_task(args, jv, args.tasks[t]);
+        const int2 tk_nxt = (t + 1 < jv.t1) ? args.tasks[t + 1] : make_int2(0, -1);
+        const TaskView tv = decode_task(args, jv, tk_cur);
         const int kv = tv.kv, q = tv.q;
         const bool diag = args.causal && (kv == q);
         for (int sub = 0; sub < NSUB; ++sub, ++x) {
@@ -701,27 +708,37 @@ __global__ void __launch_bounds__(512, 1)
               ptx::mbar_arrive(&bars[B_S_EMPTY]);
             }
             uint32_t pk[16], dk2[16];
-            const int mask_from = diag ? (row - sub * BR - cc0) : -1;  // mask cols c < mask_from
+            // P = exp2(S*scale*log2e - L*log2e), dS = P o (dP - D), packed to bf16.
+            // The causal mask (key row > query row) exists only on the diagonal
+            // task; off the diagonal the per-element compare/select is skipped.
+            auto smx = [&](auto masked) {
+              constexpr bool MASKED = decltype(masked)::value;
+              const int mask_from = row - sub * BR - cc0;  // masked: cols c < mask_from
 #pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) {
-              const float4 l4 = *reinterpret_cast<const float4*>(Lrow + cc0 + c4 * 4);
-              const float4 d4 = *reinterpret_cast<const float4*>(Drow + cc0 + c4 * 4);
-              const float Lv[4] = {l4.x, l4.y, l4.z, l4.w};
-              const float Dv[4] = {d4.x, d4.y, d4.z, d4.w};
-              float p[4], ds[4];
+              for (int c4 = 0; c4 < 8; ++c4) {
+                const float4 l4 = *reinterpret_cast<const float4*>(Lrow + cc0 + c4 * 4);
+                const float4 d4 = *reinterpret_cast<const float4*>(Drow + cc0 + c4 * 4);
+                const float Lv[4] = {l4.x, l4.y, l4.z, l4.w};
+                const float Dv[4] = {d4.x, d4.y, d4.z, d4.w};
+                float p[4], ds[4];
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int c = c4 * 4 + e;
-                float pv = fast_exp2(fmaf(s[c], args.scale_log2, Lv[e]));
-                if (c < mask_from) pv = 0.f;  // causal: key row > query row
-                p[e] = pv;
-                ds[e] = pv * (dp[c] - Dv[e]);
+                for (int e = 0; e < 4; ++e) {
+                  const int c = c4 * 4 + e;
+                  float pv = fast_exp2(fmaf(s[c], args.scale_log2, Lv[e]));
+                  if constexpr (MASKED) {
+                    if (c < mask_from) pv = 0.f;
+                  }
+                  p[e] = pv;
+                  ds[e] = pv * (dp[c] - Dv[e]);
+                }
+                pk[c4 * 2] = pack_bf16(p[0], p[1]);
+                pk[c4 * 2 + 1] = pack_bf16(p[2], p[3]);
+                dk2[c4 * 2] = pack_bf16(ds[0], ds[1]);
+                dk2[c4 * 2 + 1] = pack_bf16(ds[2], ds[3]);
               }
-              pk[c4 * 2] = pack_bf16(p[0], p[1]);
-              pk[c4 * 2 + 1] = pack_bf16(p[2], p[3]);
-              dk2[c4 * 2] = pack_bf16(ds[0], ds[1]);
-              dk2[c4 * 2 + 1] = pack_bf16(ds[2], ds[3]);
-            }
+            };
+            if (diag) smx(std::true_type{});
+            else smx(std::false_type{});
             // P^T -> TMEM buffer pb once dV of sub-tile x - NPT consumed it.
             if (ch == 0 && x >= C::NPT)
               ptx::mbar_wait(&bars[B_PT_EMPTY0 + pb], ((x / C::NPT) - 1) & 1);
@@ -748,7 +765,7 @@ __global__ void __launch_bounds__(512, 1)
           if (row == 0 && wg == 0) DASH_TRACE_MARK(4, x);
         }
         // End of a KV segment: dK/dV epilogue (local reduction done).
-        const bool seg_end = (t + 1 == jv.t1) || (task_seg(args.tasks[t + 1]) != tv.seg);
+        const bool seg_end = (t + 1 == jv.t1) || (task_seg(tk_nxt) != tv.seg);
         if (seg_end) {
           ptx::mbar_wait(&bars[B_ACC_FULL], acc_cnt & 1);
           ++acc_cnt;
@@ -780,6 +797,7 @@ __global__ void __launch_bounds__(512, 1)
           ptx::tc_fence_before();
           ptx::mbar_arrive(&bars[B_ACC_EMPTY]);
         }
+        tk_cur = tk_nxt;
       }
     }
   } else {
