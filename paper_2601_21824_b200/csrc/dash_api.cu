@@ -17,6 +17,7 @@
 #include "bwd.cuh"
 #include "dash.h"
 #include "fwd.cuh"
+#include "fwd_tc.cuh"
 #include "schedule.h"
 
 #define DASH_API extern "C" __attribute__((visibility("default")))
@@ -424,14 +425,56 @@ DASH_API int dash_attn_bwd_launches(int causal, int schedule, int deterministic)
   return 3;  // preprocess, main, dQ convert
 }
 
+namespace dash {
+namespace {
+template <int D>
+dash_status launch_fwd_tc(const dash_shape* s, const void* q, const void* k, const void* v, void* o,
+                          float* lse, int causal, cudaStream_t st) {
+  using C = FwdCfg<D>;
+  const uint64_t HD = static_cast<uint64_t>(s->heads) * D;
+  const uint64_t BN = static_cast<uint64_t>(s->batch) * s->seqlen;
+  CUtensorMap tq, tk, tv;
+  if (!(make_map_2d(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, q, HD, BN, 64, 128) &&
+        make_map_2d(&tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, k, HD, BN, 64, 128) &&
+        make_map_2d(&tv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, v, HD, BN, 64, 128)))
+    return DASH_ERR_CUDA;
+  FwdArgs a;
+  a.o = static_cast<__nv_bfloat16*>(o);
+  a.lse = lse;
+  a.B = s->batch;
+  a.N = s->seqlen;
+  a.H = s->heads;
+  a.scale_log2 = eff_scale(s) * 1.4426950408889634f;
+  a.causal = causal ? 1 : 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dash_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(C::SMEM_BYTES));
+    attr = true;
+  }
+  const dim3 grid(s->seqlen / 128, s->batch * s->heads);
+  dash_fwd_tc_kernel<D><<<grid, 256, C::SMEM_BYTES, st>>>(tq, tk, tv, a);
+  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ERR_CUDA;
+}
+}  // namespace
+}  // namespace dash
+
 DASH_API dash_status dash_attn_fwd(const dash_shape* s, const void* q, const void* k, const void* v,
                                    void* o, float* lse, int causal, void* stream) {
   if (!shape_ok(s) || !aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) ||
       !aligned16(lse))
     return DASH_ERR_INVALID_ARG;
-  const dim3 grid(s->seqlen / 64, s->batch * s->heads);
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   const float sc = eff_scale(s);
+  // tcgen05 forward (fwd_tc.cuh) unless DASH_FWD_SIMT=1 selects the fp32 SIMT
+  // kernel (fwd.cuh), kept as a second, independent GPU implementation.
+  static const int simt = [] {
+    const char* e = std::getenv("DASH_FWD_SIMT");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (!simt) return s->head_dim == 128 ? launch_fwd_tc<128>(s, q, k, v, o, lse, causal, st)
+                                       : launch_fwd_tc<64>(s, q, k, v, o, lse, causal, st);
+  const dim3 grid(s->seqlen / 64, s->batch * s->heads);
   if (s->head_dim == 128) {
     const size_t smem = 2 * 64 * 128 * 4;
     cudaFuncSetAttribute(dash_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
