@@ -248,3 +248,26 @@ def test_host_path_matches_device_path(dash, B, N, H, d, causal, schedule):
                        schedule, True, ws)
     for a, r in zip(outs, ref):
         assert torch.equal(a, r.cpu())
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_autograd_attention_matches_oracle_and_is_deterministic(dash, causal):
+    """paper_2601_21824_b200.autograd.attention (dash_attn_fwd + dash_attn_bwd
+    behind torch.autograd): gradients within the acceptance tolerance of the
+    fp64 oracle and bitwise identical across two backward passes."""
+    from paper_2601_21824_b200.autograd import attention
+    B, N, H, d = 2, 512, 3, 128
+    cpu, g = _inputs(B, N, H, d, seed=21)
+    ref = _ref(B, N, H, d, causal, seed=21)
+    grads = []
+    for _ in range(2):
+        q, k, v = (g[n].clone().requires_grad_(True) for n in ("q", "k", "v"))
+        o = attention(q, k, v, causal, "auto", True)
+        o.backward(g["do"])
+        torch.cuda.synchronize()
+        grads.append((q.grad, k.grad, v.grad))
+    assert _nerr(o, ref["o"]) <= O_TOL
+    for name, x in zip(("dq", "dk", "dv"), grads[0]):
+        assert _nerr(x, ref[name]) <= GRAD_TOL, name
+    for a, b in zip(*grads):
+        assert torch.equal(a, b)
