@@ -104,9 +104,10 @@ size_t dash_attn_bwd_workspace_bytes(const dash_shape* shape, int causal, int sc
  * dq, dk, dv are written (not accumulated); dq = bf16(scale * accumulator)
  * by a convert kernel after the main kernel.  o and lse must come from the
  * forward of the same inputs (dash_attn_fwd or any exact equivalent).
- * DASH_ERR_UNSUPPORTED: SHIFT with causal and an odd number of KV tiles
- * (AMB-10), or SHIFT needing more co-resident CTAs than the device holds
- * (n_kv for full, n_kv/2 for causal; App. B of SURVEY.md, AMB-12).
+ * SHIFT with causal and an odd number of KV tiles runs the Symmetric Shift of
+ * n_kv + 1 tiles without the phantom tile (DESIGN.md AMB-29).
+ * DASH_ERR_UNSUPPORTED: SHIFT needing more co-resident CTAs than the device
+ * holds (n_kv for full, ceil(n_kv/2) for causal; App. B of SURVEY.md, AMB-12).
  * DASH_ERR_WORKSPACE: workspace_bytes < dash_attn_bwd_workspace_bytes(). */
 dash_status dash_attn_bwd(const dash_shape* shape, const void* q, const void* k, const void* v,
                           const void* o, const void* dout, const float* lse,
@@ -150,7 +151,8 @@ dash_status dash_check_workspace(const dash_shape* shape, int causal, int schedu
  * p == NULL selects {n_heads = 2, n_sm = n_kv, c = 1, r = 1}.
  * DASH_ERR_INVALID_ARG: n_q != n_kv, n_kv < 1, c < 1 or r < 1 (positive
  * weights: Lemma 1's premise), n_sm < 1, n_heads < 1.
- * DASH_ERR_UNSUPPORTED: SHIFT causal with odd n_kv.
+ * SHIFT causal with odd n_kv: the n_kv + 1 schedule without the phantom tile
+ * (AMB-29).
  * DASH_ERR_DEADLOCK: the schedule cannot finish on n_sm SMs (SHIFT with
  * fewer SMs than a head's jobs). */
 typedef struct {
@@ -243,6 +245,12 @@ dash_status dash_attn_bwd_dump(const dash_shape* shape, const void* q, const voi
 /* Number of device kernel launches one dash_attn_bwd makes (for accounting):
  * 3 (preprocess, main, dQ convert). */
 int dash_attn_bwd_launches(int causal, int schedule, int deterministic);
+
+/* Diagnostic code behind the calling thread's most recent DASH_ERR_CUDA (0 if
+ * none yet): the cudaError_t of the failing runtime call; 10000 + cudaError_t
+ * when the launch of the main backward kernel was refused; -1 when a TMA
+ * tensor map could not be encoded (alignment / extent of a tensor). */
+int dash_last_cuda_error(void);
 
 const char* dash_status_string(dash_status s);
 const char* dash_version(void);

@@ -57,6 +57,10 @@ class Deadlock(RuntimeError):
 class Job:
     """One SM's contiguous work: an ordered list of (kv, q) tasks."""
     tasks: list = field(default_factory=list)  # [(i, j)], in execution order
+    # Visit step of each task in the schedule's own step numbering; None = the
+    # position in `tasks`.  Differs only for odd-n Symmetric Shift (AMB-29),
+    # whose jobs are the n+1 schedule with the phantom tile's tasks removed.
+    steps: list | None = None
 
 
 def task_exists(i: int, j: int, mask: int) -> bool:
@@ -76,9 +80,14 @@ def build_jobs(schedule: int, n: int, mask: int) -> list[Job]:
         # SM_i visits Q tiles i, i+1, ..., n-1, 0, ..., i-1 (AMB-5).
         for i in range(n):
             jobs.append(Job([(i, (i + t) % n) for t in range(n)]))
+    elif schedule == SHIFT and mask == CAUSAL and n % 2:
+        # AMB-29: odd n = the Symmetric Shift of n + 1 tiles (even) without the
+        # phantom KV tile n and the phantom Q tile n: every real task keeps the
+        # visit step it has there, so each dQ_j keeps its step order.
+        for job in build_jobs(SHIFT, n + 1, CAUSAL):
+            kept = [(t, (i, j)) for t, (i, j) in enumerate(job.tasks) if i < n and j < n]
+            jobs.append(Job([ij for _, ij in kept], [t for t, _ in kept]))
     elif schedule == SHIFT and mask == CAUSAL:
-        if n % 2:
-            raise ValueError("symmetric shift needs an even number of KV tiles (AMB-10)")
         h = n // 2
         for p in range(h):
             tasks = []
@@ -103,7 +112,8 @@ def reduction_ranks(schedule: int, n: int, mask: int) -> dict:
     jobs = build_jobs(schedule, n, mask)
     contrib: dict[int, list] = {j: [] for j in range(n)}
     for job in jobs:
-        for step, (i, j) in enumerate(job.tasks):
+        steps = job.steps if job.steps is not None else range(len(job.tasks))
+        for step, (i, j) in zip(steps, job.tasks):
             # NAIVE / DESCENDING: ascending KV order (AMB-6).
             # SHIFT: order of the visit step (Fig. 6 caption P:119).
             key = i if schedule in (NAIVE, DESCENDING) else step

@@ -60,6 +60,29 @@ int acc_split_for(int n) {
 }
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Entry of every launching ABI call.  A thread that has not used the CUDA
+// runtime yet (e.g. PyTorch's autograd worker) may have no current context;
+// the TMA tensor-map encoder validates addresses against the current context
+// and fails without one, so make the device's primary context current
+// (cudaSetDevice does, CUDA >= 12).  Also drops an error left in this thread
+// by someone else's CUDA call, so DASH_ERR_CUDA reports only this call.
+void bind_context() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaSetDevice(dev);
+  (void)cudaGetLastError();
+}
+
+// Last CUDA error behind a DASH_ERR_CUDA of this thread (dash_last_cuda_error).
+thread_local int g_last_cuda = 0;
+dash_status cuda_fail(cudaError_t e) {
+  g_last_cuda = static_cast<int>(e);
+  return DASH_ERR_CUDA;
+}
+dash_status cuda_check_last() {
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DASH_OK : cuda_fail(e);
+}
+
 // Head grouping G (bwd.cuh BwdArgs::head_group): a job covers its KV tile(s)
 // in G consecutive (b, h) heads, paying the per-job claim / refill once per G
 // heads; the heads' own schedules are untouched, so G never changes a bit
@@ -271,7 +294,10 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
             make_map_2d(&tdo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, HD, BN, 64, C::BR) &&
             make_map_2d(&tacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dqacc, D,
                         kMaxSplit * BN * static_cast<uint64_t>(s->heads), 32, C::STG_ROWS);
-  if (!ok) return DASH_ERR_CUDA;
+  if (!ok) {  // tensor map encoding (reported as -1 by dash_last_cuda_error)
+    g_last_cuda = -1;
+    return DASH_ERR_CUDA;
+  }
 
   prof_mark(stream);
   // K1: D, ticket / counter reset, dQacc zero-fill for the atomic variant.
@@ -348,8 +374,11 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tdo, tacc, a) != cudaSuccess)
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tdo, tacc, a);
+    if (le != cudaSuccess) {
+      g_last_cuda = 10000 + static_cast<int>(le);  // launch of the main kernel
       return DASH_ERR_CUDA;
+    }
   }
   prof_mark(stream);
   // K4: dQ = bf16(scale * dQacc).
@@ -363,13 +392,15 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
         deterministic ? acc_split_for(s->seqlen / 128) : 1, causal ? 1 : 0);
   }
   prof_mark(stream);
-  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ERR_CUDA;
+  return cuda_check_last();
 }
 
 }  // namespace
 }  // namespace dash
 
 using namespace dash;
+
+DASH_API int dash_last_cuda_error(void) { return g_last_cuda; }
 
 DASH_API const char* dash_status_string(dash_status s) {
   switch (s) {
@@ -454,13 +485,14 @@ dash_status launch_fwd_tc(const dash_shape* s, const void* q, const void* k, con
   }
   const dim3 grid(s->seqlen / 128, s->batch * s->heads);
   dash_fwd_tc_kernel<D><<<grid, 256, C::SMEM_BYTES, st>>>(tq, tk, tv, a);
-  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ERR_CUDA;
+  return cuda_check_last();
 }
 }  // namespace
 }  // namespace dash
 
 DASH_API dash_status dash_attn_fwd(const dash_shape* s, const void* q, const void* k, const void* v,
                                    void* o, float* lse, int causal, void* stream) {
+  bind_context();
   if (!shape_ok(s) || !aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) ||
       !aligned16(lse))
     return DASH_ERR_INVALID_ARG;
@@ -489,7 +521,7 @@ DASH_API dash_status dash_attn_fwd(const dash_shape* s, const void* q, const voi
         static_cast<const __nv_bfloat16*>(v), static_cast<__nv_bfloat16*>(o), lse, s->batch,
         s->seqlen, s->heads, sc, causal ? 1 : 0);
   }
-  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ERR_CUDA;
+  return cuda_check_last();
 }
 
 DASH_API size_t dash_attn_bwd_workspace_bytes(const dash_shape* s, int causal, int schedule,
@@ -505,6 +537,7 @@ DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const voi
                                    const void* o, const void* dout, const float* lse, void* dq,
                                    void* dk, void* dv, int causal, int schedule, int deterministic,
                                    void* workspace, size_t workspace_bytes, void* stream) {
+  bind_context();
   if (!shape_ok(s)) return DASH_ERR_INVALID_ARG;
   const void* ptrs[] = {q, k, v, o, dout, lse, dq, dk, dv, workspace};
   for (const void* p : ptrs)
@@ -701,6 +734,7 @@ DASH_API dash_status dash_attn_bwd_host(const dash_shape* s, const void* q, cons
                                         const float* lse, void* dq, void* dk, void* dv, int causal,
                                         int schedule, int deterministic, void* workspace,
                                         size_t workspace_bytes, void* stream) {
+  bind_context();
   if (!shape_ok(s)) return DASH_ERR_INVALID_ARG;
   const void* hptrs[] = {q, k, v, o, dout, lse, dq, dk, dv};
   for (const void* p : hptrs)

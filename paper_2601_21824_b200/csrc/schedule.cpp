@@ -8,6 +8,7 @@
 //   j >= h, i <  h : (j - h - i) mod h      (phase 1, cyclic rectangle)
 //   j >= h, i >= h : i                      (phase 2, right triangle)
 //   j <  h         : j - i                  (phase 2, left triangle)
+// Odd n: the n + 1 schedule without the phantom tile n (AMB-29).
 #include "schedule.h"
 
 #include <map>
@@ -47,8 +48,19 @@ bool build_schedule(int schedule, int n, int mask, ScheduleTable* out) {
         t.tasks.push_back({i, j, pos_mod(j - i, n)});
       }
     }
+  } else if (schedule == kShift && mask == kCausal && n % 2) {
+    // Odd n (AMB-29): the Symmetric Shift of n + 1 tiles without the phantom
+    // KV tile n and Q tile n.  For a real Q tile j every contributor KV <= j
+    // is real, so the n + 1 closed-form ranks are still 0..j in step order.
+    ScheduleTable e;
+    if (!build_schedule(schedule, n + 1, mask, &e)) return false;
+    t.jobs = e.jobs;
+    for (int p = 0; p < e.jobs; ++p) {
+      push_job();
+      for (int k = e.job_begin[p]; k < e.job_begin[p + 1]; ++k)
+        if (e.tasks[k].kv < n && e.tasks[k].q < n) t.tasks.push_back(e.tasks[k]);
+    }
   } else if (schedule == kShift && mask == kCausal) {
-    if (n % 2) return false;
     const int h = n / 2;
     t.jobs = h;
     for (int p = 0; p < h; ++p) {

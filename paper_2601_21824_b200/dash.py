@@ -70,6 +70,8 @@ def _load():
                                        vp, sz, vp]
     lib.dash_attn_bwd_host_workspace_bytes.restype = sz
     lib.dash_attn_bwd_host_workspace_bytes.argtypes = [SP, i, i, i]
+    lib.dash_last_cuda_error.restype = i
+    lib.dash_last_cuda_error.argtypes = []
     lib.dash_attn_bwd_host.restype = st
     lib.dash_attn_bwd_host.argtypes = [SP, vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp, sz, vp]
     lib.dash_check_workspace.restype = st
@@ -107,6 +109,8 @@ def version() -> str:
 
 def _check(status: int, what: str):
     if status != OK:
+        if status == ERR_CUDA:
+            what = f"{what} (cudaError {_lib.dash_last_cuda_error()})"
         raise DashError(status, what)
 
 

@@ -52,10 +52,6 @@ def test_status_strings_and_version(dash):
 def test_schedule_table_matches_oracle(dash, schedule, mask):
     """The product's closed-form tables equal the oracle's definition-driven ones."""
     for n in range(1, 70):
-        if schedule == dag.SHIFT and mask == dag.CAUSAL and n % 2:
-            with pytest.raises(dash.DashError):
-                dash.schedule_table(schedule, n, mask)
-            continue
         jobs = dash.schedule_table(schedule, n, mask)
         ojobs = dag.build_jobs(schedule, n, mask)
         ranks = dag.reduction_ranks(schedule, n, mask)
@@ -71,8 +67,6 @@ def test_critical_path_matches_oracle_simulator(dash):
     for schedule in (dag.NAIVE, dag.DESCENDING, dag.SHIFT):
         for mask in (dag.FULL, dag.CAUSAL):
             for n in list(range(2, 17)) + [24, 32, 48, 64]:
-                if schedule == dag.SHIFT and mask == dag.CAUSAL and n % 2:
-                    continue
                 for m in (1, 2, 3, 5):
                     for c, r in ((1, 1), (3, 1), (1, 3), (7, 4)):
                         for n_sm in {n, max(1, n // 2 + 1), n + 3}:
@@ -107,9 +101,9 @@ def test_critical_path_defaults_and_errors(dash):
         with pytest.raises(dash.DashError) as e:
             dash.schedule_critical_path(**kw)
         assert e.value.status == dash.ERR_INVALID_ARG
-    with pytest.raises(dash.DashError) as e:
-        dash.schedule_critical_path(dash.SHIFT, 5, 5, dash.CAUSAL)
-    assert e.value.status == dash.ERR_UNSUPPORTED
+    # odd n_kv Symmetric Shift (AMB-29) is defined; the model agrees with the oracle
+    assert dash.schedule_critical_path(dash.SHIFT, 5, 5, dash.CAUSAL) == \
+        dag.simulate(dag.SHIFT, 5, dag.CAUSAL, 2, 5, 1, 1)
     with pytest.raises(dash.DashError) as e:
         dash.schedule_critical_path(dash.SHIFT, 8, 8, dash.FULL, n_heads=2, n_sm=7)
     assert e.value.status == dash.ERR_DEADLOCK

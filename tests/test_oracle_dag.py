@@ -160,9 +160,7 @@ def test_longest_path_detects_cycle():
 @pytest.mark.parametrize("schedule", [NAIVE, DESCENDING, SHIFT])
 @pytest.mark.parametrize("mask", [FULL, CAUSAL])
 def test_schedule_structure(schedule, mask):
-    for n in range(2, 33, 1 if schedule != SHIFT or mask == FULL else 2):
-        if schedule == SHIFT and mask == CAUSAL and n % 2:
-            continue
+    for n in range(1, 33):
         jobs = dag.build_jobs(schedule, n, mask)
         rank = dag.reduction_ranks(schedule, n, mask)
         tasks = [t for job in jobs for t in job.tasks]
@@ -179,16 +177,26 @@ def test_schedule_structure(schedule, mask):
             rs = sorted(rank[(i, jj)] for (i, jj) in expect if jj == j)
             assert rs == list(range(len(rs)))
         if schedule == SHIFT:
-            steps = max(len(job.tasks) for job in jobs)
-            assert all(len(job.tasks) == steps for job in jobs)  # balanced chains
-            if mask == CAUSAL:
-                assert steps == n + 1  # n + 1 tasks per symmetric pair
-            for t in range(steps):  # conflict-free: distinct Q tiles per step
-                js = [job.tasks[t][1] for job in jobs]
+            def steps_of(job):
+                return job.steps if job.steps is not None else list(range(len(job.tasks)))
+            odd = mask == CAUSAL and n % 2
+            if not odd:
+                steps = max(len(job.tasks) for job in jobs)
+                assert all(len(job.tasks) == steps for job in jobs)  # balanced chains
+                if mask == CAUSAL:
+                    assert steps == n + 1  # n + 1 tasks per symmetric pair
+            else:  # AMB-29: the n + 1 schedule minus the phantom tile's tasks
+                assert len(jobs) == (n + 1) // 2
+                assert all(steps_of(job) == sorted(steps_of(job)) for job in jobs)
+            by_t = {}
+            for job in jobs:
+                for t, (i, j) in zip(steps_of(job), job.tasks):
+                    by_t.setdefault(t, []).append(j)
+            for js in by_t.values():  # conflict-free: distinct Q tiles per step
                 assert len(set(js)) == len(js)
             for j in range(n):  # ranks strictly increase with the visit step
                 by_step = sorted((t, rank[(i, jj)]) for job in jobs
-                                 for t, (i, jj) in enumerate(job.tasks) if jj == j)
+                                 for t, (i, jj) in zip(steps_of(job), job.tasks) if jj == j)
                 assert [rk for _, rk in by_step] == list(range(len(by_step)))
         else:
             for (i, j), rk in rank.items():
