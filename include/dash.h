@@ -106,8 +106,11 @@ size_t dash_attn_bwd_workspace_bytes(const dash_shape* shape, int causal, int sc
  * forward of the same inputs (dash_attn_fwd or any exact equivalent).
  * SHIFT with causal and an odd number of KV tiles runs the Symmetric Shift of
  * n_kv + 1 tiles without the phantom tile (DESIGN.md AMB-29).
+ * SHIFT with the full mask and n_kv > 128 runs in groups of <= 128 KV tiles
+ * (AMB-30).
  * DASH_ERR_UNSUPPORTED: SHIFT needing more co-resident CTAs than the device
- * holds (n_kv for full, ceil(n_kv/2) for causal; App. B of SURVEY.md, AMB-12).
+ * holds (min(n_kv, 128-tile group) for full, ceil(n_kv/2) for causal; App. B of
+ * SURVEY.md, AMB-12).
  * DASH_ERR_WORKSPACE: workspace_bytes < dash_attn_bwd_workspace_bytes(). */
 dash_status dash_attn_bwd(const dash_shape* shape, const void* q, const void* k, const void* v,
                           const void* o, const void* dout, const float* lse,

@@ -63,6 +63,9 @@ class Job:
     steps: list | None = None
 
 
+SHIFT_GROUP = 128  # AMB-30: largest group of KV tiles in one cyclic shift
+
+
 def task_exists(i: int, j: int, mask: int) -> bool:
     return mask == FULL or j >= i
 
@@ -78,8 +81,15 @@ def build_jobs(schedule: int, n: int, mask: int) -> list[Job]:
             jobs.append(Job([(i, j) for j in reversed(range(n)) if task_exists(i, j, mask)]))
     elif schedule == SHIFT and mask == FULL:
         # SM_i visits Q tiles i, i+1, ..., n-1, 0, ..., i-1 (AMB-5).
-        for i in range(n):
-            jobs.append(Job([(i, (i + t) % n) for t in range(n)]))
+        # AMB-30: more than SHIFT_GROUP KV tiles -> G = ceil(n / SHIFT_GROUP)
+        # consecutive near-equal groups; dQ_j takes group 0's contributions
+        # first, then group 1's, ..., each group in visit-step order.  The step
+        # label (group, t) carries that order.
+        G = -(-n // SHIFT_GROUP)
+        for g in range(G):
+            for i in range(g * n // G, (g + 1) * n // G):
+                tasks = [(i, (i + t) % n) for t in range(n)]
+                jobs.append(Job(tasks, [(g, t) for t in range(n)] if G > 1 else None))
     elif schedule == SHIFT and mask == CAUSAL and n % 2:
         # AMB-29: odd n = the Symmetric Shift of n + 1 tiles (even) without the
         # phantom KV tile n and the phantom Q tile n: every real task keeps the

@@ -273,7 +273,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     return e ? std::atoi(e) : 0;
   }();
 
-  if (schedule == kShift && tab->jobs > grid) return DASH_ERR_UNSUPPORTED;
+  if (schedule == kShift && tab->coresident > grid) return DASH_ERR_UNSUPPORTED;
   const DevTable* dt = device_table(dev, tab, G);
   if (!dt) return DASH_ERR_CUDA;
 

@@ -11,6 +11,7 @@
 // Odd n: the n + 1 schedule without the phantom tile n (AMB-29).
 #include "schedule.h"
 
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <queue>
@@ -40,12 +41,27 @@ bool build_schedule(int schedule, int n, int mask, ScheduleTable* out) {
       }
     }
   } else if (schedule == kShift && mask == kFull) {
+    // Groups of KV tiles [lo, hi), G = ceil(n / kShiftGroup) near-equal groups
+    // (one group = the paper's cyclic shift, whenever n <= kShiftGroup).
+    // KV i visits Q (i + s) mod n; dQ_j is reduced group by group, inside a
+    // group in visit-step order (AMB-30):
+    //   rank(i, j) = lo + (i <= j ? min(hi-1, j) - i : cnt_le + hi - 1 - i),
+    //   cnt_le = #{group members <= j}.   (G = 1: rank = (j - i) mod n.)
     t.jobs = n;
-    for (int i = 0; i < n; ++i) {
-      push_job();
-      for (int s = 0; s < n; ++s) {
-        const int j = (i + s) % n;
-        t.tasks.push_back({i, j, pos_mod(j - i, n)});
+    const int G = (n + kShiftGroup - 1) / kShiftGroup;
+    for (int g = 0; g < G; ++g) {
+      const int lo = static_cast<int>(static_cast<int64_t>(g) * n / G);
+      const int hi = static_cast<int>(static_cast<int64_t>(g + 1) * n / G);
+      t.coresident = std::max(t.coresident, hi - lo);
+      for (int i = lo; i < hi; ++i) {
+        push_job();
+        for (int s = 0; s < n; ++s) {
+          const int j = (i + s) % n;
+          const int top = std::min(hi - 1, j);
+          const int cnt_le = std::max(0, top - lo + 1);
+          const int rank = lo + (i <= j ? top - i : cnt_le + (hi - 1 - i));
+          t.tasks.push_back({i, j, rank});
+        }
       }
     }
   } else if (schedule == kShift && mask == kCausal && n % 2) {
@@ -55,6 +71,7 @@ bool build_schedule(int schedule, int n, int mask, ScheduleTable* out) {
     ScheduleTable e;
     if (!build_schedule(schedule, n + 1, mask, &e)) return false;
     t.jobs = e.jobs;
+    t.coresident = e.coresident;
     for (int p = 0; p < e.jobs; ++p) {
       push_job();
       for (int k = e.job_begin[p]; k < e.job_begin[p + 1]; ++k)
@@ -63,6 +80,7 @@ bool build_schedule(int schedule, int n, int mask, ScheduleTable* out) {
   } else if (schedule == kShift && mask == kCausal) {
     const int h = n / 2;
     t.jobs = h;
+    t.coresident = h;
     for (int p = 0; p < h; ++p) {
       push_job();
       for (int s = 0; s <= n; ++s) {

@@ -22,13 +22,18 @@ struct ScheduleTable {
   int n = 0;
   int schedule = 0, mask = 0;
   int jobs = 0;                   // jobs per head (n, or n/2 for SHIFT causal)
+  int coresident = 0;             // SHIFT: jobs that must be co-resident (largest group)
   std::vector<int32_t> job_begin;  // jobs + 1 offsets into tasks
   std::vector<Task> tasks;         // per job, in visiting order
   int max_rank_plus1(int j) const;  // contributions to dQ_j (n or j+1)
 };
 
-// Returns false (and leaves *out empty) for an unsupported combination
-// (SHIFT causal with odd n).
+// SHIFT full with more than kShiftGroup KV tiles runs in groups of at most
+// kShiftGroup tiles (AMB-30): a fixed constant, so tables never depend on the
+// device.
+constexpr int kShiftGroup = 128;
+
+// Returns false (and leaves *out empty) for an unsupported combination.
 bool build_schedule(int schedule, int n, int mask, ScheduleTable* out);
 
 // Shared, thread-safe cache of built tables keyed by (schedule, n, mask).

@@ -51,7 +51,7 @@ def test_status_strings_and_version(dash):
 @pytest.mark.parametrize("mask", [dag.FULL, dag.CAUSAL])
 def test_schedule_table_matches_oracle(dash, schedule, mask):
     """The product's closed-form tables equal the oracle's definition-driven ones."""
-    for n in range(1, 70):
+    for n in list(range(1, 70)) + [129, 257]:  # + grouped SHIFT full (AMB-30)
         jobs = dash.schedule_table(schedule, n, mask)
         ojobs = dag.build_jobs(schedule, n, mask)
         ranks = dag.reduction_ranks(schedule, n, mask)

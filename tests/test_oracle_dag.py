@@ -238,3 +238,31 @@ def test_default_params_separate_the_schedules():
         assert dag.simulate(DESCENDING, n, CAUSAL) == 3 * n + 1
         assert dag.simulate(SHIFT, n, FULL) == 4 * n
         assert dag.simulate(SHIFT, n, CAUSAL) == 2 * n + 2
+
+
+def test_grouped_shift_full_beyond_group_size():
+    """AMB-30: SHIFT with the full mask and more than SHIFT_GROUP KV tiles runs in
+    near-equal groups; inside a group the cyclic shift is conflict-free and each
+    dQ_j is reduced group-major, in visit-step order inside a group."""
+    for n in (129, 200, 257):
+        jobs = dag.build_jobs(SHIFT, n, FULL)
+        rank = dag.reduction_ranks(SHIFT, n, FULL)
+        G = -(-n // dag.SHIFT_GROUP)
+        sizes = {}
+        for job in jobs:
+            g = job.steps[0][0]
+            sizes[g] = sizes.get(g, 0) + 1
+            assert len(job.tasks) == n
+        assert len(sizes) == G and max(sizes.values()) <= dag.SHIFT_GROUP
+        assert max(sizes.values()) - min(sizes.values()) <= 1
+        by_label = {}
+        for job in jobs:
+            for lab, (i, j) in zip(job.steps, job.tasks):
+                by_label.setdefault(lab, []).append(j)
+        assert all(len(set(js)) == len(js) for js in by_label.values())  # conflict-free
+        for j in (0, 1, n // 2, n - 1):
+            order = sorted((lab, i) for job in jobs for lab, (i, jj) in zip(job.steps, job.tasks)
+                           if jj == j)
+            assert [rank[(i, j)] for _, i in order] == list(range(n))
+        # the model finishes with one group's worth of SMs (co-residency of a group)
+        assert dag.simulate(SHIFT, n, FULL, 1, max(sizes.values()), 2, 1) > 0
