@@ -62,6 +62,7 @@ SHAPES = [
     (1, 384, 2, 64),    # odd number of KV tiles
     (1, 1024, 2, 128),
     (3, 256, 5, 64),
+    (2, 128, 3, 128),   # a single KV tile (n = 1): the degenerate schedule
 ]
 
 
