@@ -222,6 +222,55 @@ def cpu_oracle_sample(head_dim, causal, heads=None):
                       f"{'causal' if causal else 'full'}), FLOPs by the FA convention"}
 
 
+def oracle_timing(out_path):
+    """The CPU baseline beside the GPU: the fp64 oracle as it
+    stands on this host -- config 1 single-thread and all-core, one bounded sample
+    of the N = 512 / 2048 sweep shapes per mask (scaled to the full shape), one
+    head of N = 4096 for the long-context config (extrapolated, labelled)."""
+    import platform
+    import oracle
+    from paper_2601_21824_b200.inputs import attn_inputs
+    oracle.build()
+    cores = len(os.sched_getaffinity(0))
+    cpu = platform.machine()
+    try:
+        with open("/proc/cpuinfo") as fh:
+            cpu = next(l.split(":", 1)[1].strip() for l in fh if l.startswith("model name"))
+    except (OSError, StopIteration):
+        pass
+
+    def run(B, N, H, d, causal, threads):
+        oracle.set_threads(threads)
+        x = attn_inputs(B, N, H, d, seed=0)
+        f = {k: v.double().numpy() for k, v in x.items()}
+        t = time.time()
+        oracle.attn_bwd(f["q"], f["k"], f["v"], f["do"], causal)
+        dt = time.time() - t
+        return dt, fa_flops(B, N, H, d, causal) / dt / 1e12
+
+    res = {"cpu_model": cpu, "cores": cores, "rows": []}
+    for causal in (True, False):
+        for threads in (1, cores):
+            dt, tf = run(1, 256, 1, 64, causal, threads)
+            res["rows"].append({"config": "1 (B=1,H=1,N=256,d=64)", "causal": causal,
+                                "threads": threads, "seconds": dt, "tflops": tf})
+    for N, heads in ((512, 4 * cores), (2048, cores)):
+        for causal in (True, False):
+            dt, tf = run(1, N, heads, 128, causal, cores)
+            B, H = TOKENS // N, HIDDEN // 128
+            res["rows"].append({"config": f"sweep N={N} d=128 ({heads} of {B * H} heads)",
+                                "causal": causal, "threads": cores, "seconds": dt, "tflops": tf,
+                                "extrapolated_full_shape_seconds": dt * B * H / heads})
+    dt, tf = run(1, 4096, 1, 128, True, cores)  # one head runs on one thread
+    res["rows"].append({"config": "4 long context (B=8,H=32,N=32768,d=128 causal), from one head of N=4096",
+                        "causal": True, "threads": 1, "seconds": dt, "tflops": tf,
+                        "extrapolated_full_config_seconds": dt * 64 * 256 / cores,
+                        "note": "extrapolated: x64 (N^2) x 256 heads / cores threads; not measured"})
+    with open(out_path, "w") as fh:
+        json.dump(res, fh, indent=1)
+    print(json.dumps(res), flush=True)
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -298,6 +347,10 @@ def main():
     ap.add_argument("--no-sweep", action="store_true", help="skip the per-schedule sweep table")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--oracle-timing", default=None, metavar="OUT.json",
+                    help="cpu_baseline leg only: time the fp64 oracle on config 1 "
+                         "(single thread / all cores), the N = 512 and 2048 sweep shapes and "
+                         "one long-context head (extrapolated), write OUT.json, exit")
     ap.add_argument("--seqlens", default=None,
                     help="comma-separated subset of the sweep (profiling only; not a bench line)")
     args = ap.parse_args()
@@ -306,6 +359,9 @@ def main():
         args.schedule = "auto"
     if args.impl == "reference":
         bench_reference(args)
+        return
+    if args.oracle_timing:
+        oracle_timing(args.oracle_timing)
         return
 
     import torch

@@ -1,7 +1,7 @@
 """BASELINE.json config 4: long context -- B = 8, H = 32, N = 32768, d = 128,
 causal.  Times dash_attn_bwd under NAIVE / DESCENDING / SHIFT (deterministic)
-and the atomic variant, and checks sampled dQ rows of two heads against the
-fp64 oracle (computed one row at a time).
+and the atomic variant (measurement only; the sampled-row parity of this
+configuration is a GPU test, tests/test_gpu_bwd.py).
 
   python scripts/long_context.py [--out profiles/r01_long_context.json] [--batch 8]
 """
@@ -10,12 +10,10 @@ import json
 import os
 import sys
 
-import numpy as np
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-import oracle  # noqa: E402  (sampled parity only)
 from paper_2601_21824_b200 import dash  # noqa: E402
 from paper_2601_21824_b200.inputs import attn_inputs  # noqa: E402
 
@@ -51,14 +49,8 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.reps
         res[name] = {"ms": ms, "tflops": flops / (ms / 1e3) / 1e12}
-        if name == "auto":
-            dq = out[0]
-            f = {k: v[:1].double().numpy() for k, v in cpu.items()}  # batch 0 only
-            heads, rows = [0, 31], [0, 4097, 20000, 32767]
-            ref = oracle.attn_bwd_dq_rows(f["q"], f["k"], f["v"], f["do"], True, heads, rows)
-            got = np.stack([dq[0, rows, h].float().cpu().numpy() for h in heads])
-            res["auto"]["sampled_dq_err_normalised"] = float(
-                np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
+    # parity of this configuration against the fp64 oracle lives in
+    # tests/test_gpu_bwd.py::test_long_context_config4_sampled_rows (sampled rows)
     res["deadlock_check"] = dash.check_workspace(g["q"].shape, True, "shift", True, ws)
     gap = res["atomic"]["tflops"] - res["naive"]["tflops"]
     best = max(res["shift"]["tflops"], res["descending"]["tflops"])
