@@ -494,6 +494,16 @@ def main():
                 else:
                     row["gap_closed" + suffix] = (best - row["naive" + suffix]) / gap
                     row["pass" + suffix] = row["gap_closed" + suffix] >= 0.5
+            # Against the paper's own baseline: FA3-style NAIVE with one ordered
+            # accumulator per dQ tile (W = 1), DASH schedules at
+            # the library's W (AMB-27 is part of this build's ordered reduction).
+            if row.get("naive_w1") is not None and row.get("best_dash") is not None:
+                gap = row["atomic"] - row["naive_w1"]
+                row["gap_closed_vs_fa3_naive"] = ((row["best_dash"] - row["naive_w1"]) / gap
+                                                  if gap >= 0.02 * row["atomic"] else None)
+                row["pass_vs_fa3_naive"] = (row["gap_closed_vs_fa3_naive"] >= 0.5
+                                            if row["gap_closed_vs_fa3_naive"] is not None
+                                            else row["best_dash"] >= 0.98 * row["naive_w1"])
             sweep.append(row)
 
     cpu = None
