@@ -16,9 +16,13 @@
  *  - Supported: d in {64, 128}; N a positive multiple of 128 (the KV/Q tile
  *    size B_r = B_c = 128 of the schedule model, AMB-11); seqlen_q = seqlen_k.
  *  - softmax_scale <= 0 selects 1/sqrt(d) (AMB-1).
- *  - Device pointers are CUDA device pointers owned by the caller.  The
- *    library never allocates device memory; all scratch lives in the
- *    caller-provided workspace.  `stream` is a cudaStream_t (NULL = legacy
+ *  - Device pointers are CUDA device pointers owned by the caller.  All
+ *    scratch lives in the caller-provided workspace; the only device memory
+ *    the library allocates is its schedule tables (a few KB per (device,
+ *    schedule, n, mask), uploaded once on first use and cached), and
+ *    dash_attn_bwd_host creates three library-owned streams per device on
+ *    first use.  After a warm-up call the backward can be captured in a CUDA
+ *    graph.  `stream` is a cudaStream_t (NULL = legacy
  *    default stream); every call is stream-ordered and asynchronous unless
  *    stated otherwise.  A workspace must not be used by two in-flight calls.
  *  - Errors are returned as dash_status; nothing is thrown across the ABI.
