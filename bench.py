@@ -348,7 +348,7 @@ def main():
     ap.add_argument("--schedule", default=None,
                     help="naive | descending | shift | auto (default: auto, the library's per-shape choice)")
     ap.add_argument("--acc-split", type=int, default=None,
-                    help="interleaved dQ accumulators W in {1,2,4} (AMB-27); default: the library's automatic choice")
+                    help="interleaved dQ accumulators W in {1,2,4,8} (AMB-27); default: the library's automatic choice")
     ap.add_argument("--no-sweep", action="store_true", help="skip the per-schedule sweep table")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--no-e2e", action="store_true")

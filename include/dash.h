@@ -87,10 +87,11 @@ typedef struct {
 dash_status dash_attn_fwd(const dash_shape* shape, const void* q, const void* k, const void* v,
                           void* o, float* lse, int causal, void* stream);
 
-/* Bytes of device workspace dash_attn_bwd needs for this problem: the fp32
- * dQ accumulator [B,H,N,d] (Alg.1 line 34's "dQ_i in global memory"),
+/* Bytes of device workspace dash_attn_bwd needs for this problem: room for
+ * the largest W = 8 interleaved fp32 dQ accumulators [8][B,H,N,d] (Alg.1
+ * line 34's "dQ_i in global memory"; AMB-27),
  * D = rowsum(dO o O) fp32 [B,H,N] (Alg.1 line 1; AMB-2), one int32
- * ticket per (b, h, Q sub-tile) (the "global order"), the job
+ * ticket per (W, b, h, Q sub-tile) (the "global order"), the job
  * counter and the schedule table.  Returns 0 for an invalid shape. */
 size_t dash_attn_bwd_workspace_bytes(const dash_shape* shape, int causal, int schedule,
                                      int deterministic);
@@ -223,9 +224,9 @@ int dash_attn_bwd_resolve_schedule(const dash_shape* shape, int causal, int sche
  * accumulator are W schedule steps apart instead of one.
  * dash_attn_bwd_acc_split(seqlen) returns the W a call with that N uses
  * (seqlen not a positive multiple of 128: returns the setting itself, 0 =
- * automatic).  The setting defaults to automatic (W = 4 for N >= 8192, else
- * 2; depends on N only), or to the DASH_ACC_SPLIT environment variable.
- * dash_attn_bwd_set_acc_split(w), w in {0 (automatic), 1, 2, 4}, changes it
+ * automatic).  The setting defaults to automatic (W = 8 for N >= 32768, 4 for
+ * N >= 8192, else 2; depends on N only), or to the DASH_ACC_SPLIT environment variable.
+ * dash_attn_bwd_set_acc_split(w), w in {0 (automatic), 1, 2, 4, 8}, changes it
  * for later calls (host-global, not for concurrent use; other values:
  * DASH_ERR_INVALID_ARG).  The atomic variant always uses one accumulator. */
 int dash_attn_bwd_acc_split(int seqlen);

@@ -28,11 +28,11 @@ namespace {
 constexpr size_t kAlign = 1024;
 constexpr int kDefaultVariant = 3;  // BwdCfg smem variant used unless DASH_VARIANT is set
 // Interleaved dQ accumulators (AMB-27): 0 = automatic (the default), else
-// fixed W in {1, 2, 4}; DASH_ACC_SPLIT overrides the default at load time.
+// fixed W in {1, 2, 4, 8}; DASH_ACC_SPLIT overrides the default at load time.
 int g_acc_split = [] {
   const char* e = std::getenv("DASH_ACC_SPLIT");
   const int v = e ? std::atoi(e) : 0;
-  return (v == 1 || v == 2 || v == 4) ? v : 0;
+  return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 0;
 }();
 int acc_split() { return g_acc_split; }
 // DASH_SCHED_AUTO: the paper's schedule that measured fastest on B200 for
@@ -50,13 +50,14 @@ int auto_schedule(const dash_shape* s, int causal) {
 }
 
 // W actually used for a problem with n 128-row tiles per head.  Automatic:
-// W = 4 once the per-tile chain is long (n >= 64), else 2 -- measured on
-// B200 (profiles/r01_experiments/acc_split.txt): extra accumulators cost the
-// convert kernel one more fp32 read each, which only pays off at long
-// sequences.  Depends on n only, so (b, h) sharding never changes it.
+// W = 4 once the per-tile chain is long (n >= 64), W = 8 from n >= 256
+// (N >= 32k), else 2 -- measured on B200 (profiles/r01_experiments/acc_split.txt,
+// acc_split_w8.txt): extra accumulators cost the convert kernel one more fp32
+// read each, which only pays off at long sequences.  Depends on n only, so
+// (b, h) sharding never changes it.
 int acc_split_for(int n) {
   if (g_acc_split) return g_acc_split;
-  return n >= 64 ? 4 : 2;
+  return n >= 256 ? 8 : n >= 64 ? 4 : 2;
 }
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -121,7 +122,7 @@ struct WsLayout {
 };
 // Up to kMaxSplit interleaved fp32 accumulators (AMB-27), each with its own
 // ticket set: dqacc [W][B,H,N,d], tickets [W][B*H][N / ticket_rows].
-constexpr int kMaxSplit = 4;
+constexpr int kMaxSplit = 8;
 WsLayout ws_layout(const dash_shape* s) {
   WsLayout w;
   const size_t BHN = static_cast<size_t>(s->batch) * s->heads * s->seqlen;
@@ -591,7 +592,7 @@ DASH_API int dash_attn_bwd_acc_split(int seqlen) {
 }
 
 DASH_API dash_status dash_attn_bwd_set_acc_split(int w) {
-  if (w != 0 && w != 1 && w != 2 && w != 4) return DASH_ERR_INVALID_ARG;
+  if (w != 0 && w != 1 && w != 2 && w != 4 && w != 8) return DASH_ERR_INVALID_ARG;
   g_acc_split = w;
   return DASH_OK;
 }

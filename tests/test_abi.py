@@ -156,8 +156,8 @@ def test_auto_schedule_policy_and_acc_split(dash):
     old = dash.acc_split()
     try:
         dash.set_acc_split(0)
-        assert [dash.acc_split(N) for N in (512, 4096, 8192, 32768)] == [2, 2, 4, 4]
-        for w in (1, 2, 4):
+        assert [dash.acc_split(N) for N in (512, 4096, 8192, 16384, 32768)] == [2, 2, 4, 4, 8]
+        for w in (1, 2, 4, 8):
             dash.set_acc_split(w)
             assert dash.acc_split(1024) == w and dash.acc_split() == w
         with pytest.raises(dash.DashError):

@@ -40,7 +40,7 @@ def bf16_rn_bits(x32: np.ndarray) -> np.ndarray:
     return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
 
 
-@pytest.fixture(params=[1, 2, 4], ids=lambda w: f"W{w}")
+@pytest.fixture(params=[1, 2, 4, 8], ids=lambda w: f"W{w}")
 def acc_split(request, dash):
     """Run the test under W interleaved accumulators (AMB-27), then restore."""
     old = dash.acc_split()
