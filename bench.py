@@ -20,10 +20,21 @@ roofline  = the main kernel's algorithmic tile FLOPs (5 GEMMs of 2*128*128*d
             time, against MEASURED_PEAKS.json bf16_tflops.
 sweep     = per-seqlen TFLOP/s of NAIVE / DESCENDING / SHIFT (deterministic)
             and the atomic variant, with the gap-closure ratio (AMB-19).
+gate      = the north_star target per swept shape for configs 2 and 3
+            (causal HD128, full HD128, full HD64, causal HD64): the best of
+            DESCENDING / SHIFT against NAIVE at the SAME number W of
+            interleaved accumulators (AMB-27) -- the primary reading -- and
+            at W = 1 (the paper's single accumulator) beside it.
 
-Multi-GPU (torchrun): weak scaling -- every rank owns H (b, h) heads of a
-G*H-head problem (sharding by heads needs no collective, SURVEY §8(e));
-value = all ranks' FLOPs / max-over-ranks time.
+Multi-GPU (`--gpus N`; launched under torchrun, or re-executes itself under
+torch.distributed.run when started bare): strong scaling by default -- the
+fixed sweep problem is split over the U = B*H flattened (b, h) units, rank r
+owning the contiguous range [r*U/N, (r+1)*U/N); no collective
+on the data path; value = the whole problem's FLOPs / max-over-ranks device
+time.  After timing, per-unit SHA-256 digests of dq/dk/dv are all-gathered
+(NCCL) and rank 0 checks them against its own 1-GPU run of the whole problem
+(`sharding_bitwise_identical`).  `--scaling weak` instead gives every rank a
+full problem of its own (per-rank seeds).
 
 --impl reference times the fp64 CPU oracle (oracle/, the correctness
 reference; there is no runnable upstream implementation) on a bounded sample
@@ -134,11 +145,32 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # CPU tests of the plumbing (gloo)
+            dist.init_process_group("gloo")
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
+
+
+def relaunch_if_needed(args):
+    """`--gpus N` (N > 1) without a torchrun environment: re-execute this
+    command under torch.distributed.run with N ranks on 127.0.0.1; under
+    torchrun, the world size must equal N."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
+    if world is not None and int(world) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
 
 def barrier(world):
@@ -152,22 +184,74 @@ def max_over_ranks(x, world):
     if world == 1:
         return x
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
 
-def make_problem(B, N, H, d, causal, rank, dash, torch):
+def shard_inputs(cpu, world, rank, scaling):
+    """Rank's inputs: strong scaling -> its flattened (b, h) units of the
+    shared problem (paper_2601_21824_b200.dist.shard_units); weak -> all of it."""
+    if scaling == "weak" or world == 1:
+        return dict(cpu)
+    from paper_2601_21824_b200 import dist as ddist
+    return {k: ddist.shard_units(v, world, rank) for k, v in cpu.items()}
+
+
+def make_problem(B, N, H, d, causal, rank, world, scaling, dash, torch):
     from paper_2601_21824_b200.inputs import attn_inputs
-    # weak scaling: rank r owns heads [r*H, (r+1)*H) of a (world*H)-head problem;
-    # drawing a per-rank seed keeps host memory per process bounded.
-    cpu = attn_inputs(B, N, H, d, seed=1000 * rank + N)
+    # strong: every rank draws the same problem (seed N) and keeps its units;
+    # weak: rank r draws its own full problem (seed 1000 r + N).
+    seed = N if scaling == "strong" else 1000 * rank + N
+    cpu = shard_inputs(attn_inputs(B, N, H, d, seed=seed), world, rank, scaling)
     g = {k: v.cuda() for k, v in cpu.items()}
     o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], causal)
     g["o"], g["lse"] = o, lse
     g["out"] = (torch.empty_like(g["q"]), torch.empty_like(g["k"]), torch.empty_like(g["v"]))
     g["ws"] = dash.alloc_workspace(g["q"].shape, causal)
+    g["shape"] = tuple(g["q"].shape)
     return g
+
+
+def verify_sharding(world, rank, full_shapes, run_shard, run_full):
+    """Sharding check of SURVEY §8(e): per-unit SHA-256 digests of every
+    rank's outputs (run_shard(i) -> (dq, dk, dv) of its units of problem i),
+    all-gathered, must equal the digests of rank 0's run of the whole problem
+    (run_full(shape) -> (dq, dk, dv)).  Returns the verdict on rank 0, None
+    elsewhere.  bench.py passes GPU calls; tests/test_dist_gloo.py the oracle."""
+    import torch.distributed as dist
+    from paper_2601_21824_b200 import dist as ddist
+    ok = True
+    for i, shape in enumerate(full_shapes):
+        mine = [ddist.per_unit_digests(t) for t in run_shard(i)]
+        allv = [None] * world
+        dist.all_gather_object(allv, mine)
+        if rank == 0:
+            got = [sum((allv[r][t] for r in range(world)), []) for t in range(3)]
+            want = [ddist.per_unit_digests(t) for t in run_full(shape)]
+            ok = ok and got == want
+    return ok if rank == 0 else None
+
+
+def gpu_sharding_check(dash, torch, world, rank, probs, full_shapes, causal, schedule):
+    from paper_2601_21824_b200.inputs import attn_inputs
+
+    def run_shard(i):
+        out = run_bwd(dash, probs[i][1], causal, schedule, True)
+        torch.cuda.synchronize()
+        return out
+
+    def run_full(shape):
+        B, N, H, d = shape
+        full = {k: v.cuda() for k, v in attn_inputs(B, N, H, d, seed=N).items()}
+        fo, fl = dash.attn_fwd(full["q"], full["k"], full["v"], causal)
+        out = dash.attn_bwd(full["q"], full["k"], full["v"], fo, full["do"], fl, causal,
+                            schedule, True)
+        torch.cuda.synchronize()
+        return out
+
+    return verify_sharding(world, rank, full_shapes, run_shard, run_full)
 
 
 def run_bwd(dash, g, causal, schedule, det):
@@ -317,7 +401,7 @@ def bench_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * secs / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, world),
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": r["cores"], "kind": "oracle",
                          "sample": r["sample"]},
@@ -333,8 +417,82 @@ def workload_config(args, world):
             f"-{TOKENS}tok-hidden{HIDDEN}")
     return {"workload": name, "seqlens": list(SEQLENS), "total_tokens": TOKENS,
             "hidden": HIDDEN, "head_dim": args.head_dim, "mask": "causal" if causal else "full",
-            "schedule": args.schedule, "acc_split": args.acc_split, "per_gpu_heads_x_batch": [list(s[::2]) for s in shapes(args.head_dim)],
-            "parallelism": f"bh-shard x{world}", "l2": "inputs > L2 (5 x 64 MiB per sweep point, 126 MB L2)"}
+            "schedule": args.schedule, "acc_split": args.acc_split,
+            "batch_x_heads": [list(s[::2]) for s in shapes(args.head_dim)],
+            "parallelism": f"bh-units x{world} ({args.scaling})",
+            "l2": "inputs > L2 (5 x 64 MiB per sweep point, 126 MB L2)"}
+
+
+def gap_gate(naive, best, atomic):
+    """AMB-19: (gap closed, pass) of `best` over `naive` towards `atomic`."""
+    gap = atomic - naive
+    if gap < 0.02 * atomic:  # no gap (or NAIVE at / above atomic): stay within 2 %
+        return None, best >= 0.98 * naive
+    closed = (best - naive) / gap
+    return closed, closed >= 0.5
+
+
+def sweep_rows(dash, torch, probs, causal, steps):
+    """Per sweep point: NAIVE / DESCENDING / SHIFT (deterministic) and the
+    atomic variant at the library's W, and the three schedules at W = 1;
+    SWEEP_ROUNDS interleaved rounds, median per case.  The north_star gate is
+    evaluated at the SAME W on both sides (primary) and at W = 1."""
+    rows = []
+    w_bench = dash.acc_split()
+    for s, g in probs:
+        row = {"seqlen": s[1], "batch": s[0], "heads": s[2], "acc_split": dash.acc_split(s[1]),
+               "auto": dash.resolve_schedule(s, causal, "auto")}
+        f = fa_flops(*s, causal)
+        cases = [("naive", "naive", True, w_bench), ("descending", "descending", True, w_bench),
+                 ("shift", "shift", True, w_bench), ("atomic", "naive", False, w_bench)]
+        if dash.acc_split(s[1]) != 1:
+            cases += [("naive_w1", "naive", True, 1), ("descending_w1", "descending", True, 1),
+                      ("shift_w1", "shift", True, 1)]
+        # Round-robin over the cases, median per case: every schedule sees
+        # the same clock / power history.
+        times = {name: [] for name, *_ in cases}
+        nst = max(3, steps)
+        for _ in range(SWEEP_ROUNDS):
+            for name, sched, det, w in cases:
+                if row.get(name + "_error"):
+                    continue
+                dash.set_acc_split(w)
+                try:
+                    times[name].append(time_steps(
+                        torch, lambda: run_bwd(dash, g, causal, sched, det), nst, 2, 1))
+                except dash.DashError as e:
+                    row[name + "_error"] = str(e)
+        dash.set_acc_split(w_bench)
+        for name, *_ in cases:
+            row[name] = (f * nst / (statistics.median(times[name]) / 1e3) / 1e12
+                         if times[name] and not row.get(name + "_error") else None)
+        row["rounds"] = SWEEP_ROUNDS
+        for suffix in ("", "_w1"):
+            cands = [v for v in (row.get("descending" + suffix), row.get("shift" + suffix))
+                     if v is not None]
+            if row.get("naive" + suffix) is None or row.get("atomic") is None or not cands:
+                continue
+            best = max(cands)
+            row["best_dash" + suffix] = best
+            row["gap_closed" + suffix], row["pass" + suffix] = gap_gate(
+                row["naive" + suffix], best, row["atomic"])
+        # Secondary column (mixes mechanisms): DASH at the library's W against
+        # the paper's FA3-style NAIVE with one accumulator (W = 1); the
+        # difference includes the interleaved accumulators of AMB-27.
+        if row.get("naive_w1") is not None and row.get("best_dash") is not None:
+            row["gap_closed_incl_amb27"], row["pass_incl_amb27"] = gap_gate(
+                row["naive_w1"], row["best_dash"], row["atomic"])
+        rows.append(row)
+    return rows
+
+
+def gate_summary(rows):
+    return {"pass_same_w": [r.get("pass") for r in rows],
+            "gap_closed_same_w": [None if r.get("gap_closed") is None else round(r["gap_closed"], 3)
+                                  for r in rows],
+            "pass_w1": [r.get("pass_w1") for r in rows],
+            "all_pass_same_w": all(bool(r.get("pass")) for r in rows),
+            "seqlens": [r["seqlen"] for r in rows]}
 
 
 def main():
@@ -349,9 +507,15 @@ def main():
                     help="naive | descending | shift | auto (default: auto, the library's per-shape choice)")
     ap.add_argument("--acc-split", type=int, default=None,
                     help="interleaved dQ accumulators W in {1,2,4,8} (AMB-27); default: the library's automatic choice")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: strong = split the fixed problem over (b, h) units (default); "
+                         "weak = a full problem per rank")
     ap.add_argument("--no-sweep", action="store_true", help="skip the per-schedule sweep table")
+    ap.add_argument("--no-gate", action="store_true",
+                    help="skip the gate tables of the other configurations (full HD128/HD64, causal HD64)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-verify", action="store_true", help="N > 1: skip the sharding digest check")
     ap.add_argument("--oracle-timing", default=None, metavar="OUT.json",
                     help="cpu_baseline leg only: time the fp64 oracle on config 1 "
                          "(single thread / all cores), the N = 512 and 2048 sweep shapes and "
@@ -362,6 +526,7 @@ def main():
     causal = not args.full
     if args.schedule is None:
         args.schedule = "auto"
+    relaunch_if_needed(args)
     if args.impl == "reference":
         bench_reference(args)
         return
@@ -377,15 +542,20 @@ def main():
     args.acc_split = dash.acc_split()  # 0 = automatic (per seqlen: sweep rows)
     d = args.head_dim
     seqlens = tuple(int(x) for x in args.seqlens.split(",")) if args.seqlens else SEQLENS
-    probs = [(s, make_problem(*s, causal, rank, dash, torch)) for s in shapes(d, seqlens)]
+    full_shapes = shapes(d, seqlens)
+    probs = [(s, make_problem(*s, causal, rank, world, args.scaling, dash, torch))
+             for s in full_shapes]
     torch.cuda.synchronize()
 
     def step():
         for _, g in probs:
             run_bwd(dash, g, causal, args.schedule, True)
 
-    flops_fa = sum(fa_flops(*s, causal) for s, _ in probs)
-    flops_tile = sum(tile_flops(*s, causal) for s, _ in probs)
+    # FLOPs of the whole job (all ranks): the full problem (strong) or one
+    # per rank (weak); per-rank FLOPs for the roofline of this rank's kernel.
+    flops_fa = sum(fa_flops(*s, causal) for s in full_shapes)
+    job_flops = flops_fa if args.scaling == "strong" else world * flops_fa
+    rank_tile = sum(tile_flops(*g["shape"], causal) for _, g in probs)
 
     # --- headline: device-timed sweep step -----------------------------------
     prof = {}
@@ -403,11 +573,11 @@ def main():
         ms = time_steps(torch, step, args.steps, args.warmup, world, begin, end)
     ms_max = max_over_ranks(ms, world)
     _, ms_main_timed, _, ncalls = prof["ms"]  # main-kernel CUDA-event time, timed calls only
-    value = world * flops_fa * args.steps / (ms_max / 1e3) / 1e12
+    value = job_flops * args.steps / (ms_max / 1e3) / 1e12
 
     # --- roofline of the main kernel -------------------------------------------
     peak, peak_src, peak_sus = load_peaks()
-    achieved = flops_tile * args.steps / (ms_main_timed / 1e3) / 1e12
+    achieved = rank_tile * args.steps / (ms_main_timed / 1e3) / 1e12
     wl = workload_config(args, world)["workload"]
     traffic = load_traffic(wl)
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -420,18 +590,19 @@ def main():
     e2e = None
     if not args.no_e2e:
         host = []
-        for s, g in probs:
+        for _, g in probs:
             hb = {k: g[k].cpu().pin_memory() for k in ("q", "k", "v", "o", "do", "lse")}
             hb["dq"], hb["dk"], hb["dv"] = (torch.empty_like(hb["q"]).pin_memory() for _ in range(3))
-            ws = torch.empty(dash.host_workspace_bytes(s, causal), dtype=torch.uint8, device="cuda")
-            host.append((s, hb, ws))
+            ws = torch.empty(dash.host_workspace_bytes(g["shape"], causal), dtype=torch.uint8,
+                             device="cuda")
+            host.append((g["shape"], hb, ws))
         h2d = d2h = 0
-        for s, hb, _ in host:
+        for _, hb, _ in host:
             h2d += sum(hb[k].numel() * hb[k].element_size() for k in ("q", "k", "v", "o", "do", "lse"))
             d2h += sum(hb[k].numel() * hb[k].element_size() for k in ("dq", "dk", "dv"))
 
         def e2e_step():
-            for s, hb, ws in host:
+            for _, hb, ws in host:
                 dash.attn_bwd_host(hb["q"], hb["k"], hb["v"], hb["o"], hb["do"], hb["lse"], hb["dq"],
                                    hb["dk"], hb["dv"], causal, args.schedule, True, ws)
         for _ in range(max(1, args.warmup)):
@@ -444,73 +615,34 @@ def main():
         t1 = time.perf_counter()
         barrier(world)
         e2e_ms = max_over_ranks((t1 - t0) * 1e3 / steps_e2e, world)
-        e2e = {"value": world * flops_fa / (e2e_ms / 1e3) / 1e12, "unit": "TFLOP/s",
+        e2e = {"value": job_flops / (e2e_ms / 1e3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-               "steps": steps_e2e, "api": "dash_attn_bwd_host (pinned host buffers)"}
+               "steps": steps_e2e, "api": "dash_attn_bwd_host (pinned host buffers)",
+               "bytes_note": "per rank" if world > 1 else None}
         del host
 
-    # --- per-schedule sweep table (N = 1 only) ----------------------------------------
-    # Every schedule at the bench's accumulator split W (AMB-27) and at W = 1,
-    # the paper's single ordered accumulator per dQ tile, plus the atomic variant.
-    sweep = None
+    # --- sharding check (N > 1): per-unit digests vs rank 0's 1-GPU run ------------
+    sharding_ok = None
+    if world > 1 and args.scaling == "strong" and not args.no_verify:
+        sharding_ok = gpu_sharding_check(dash, torch, world, rank, probs, full_shapes, causal,
+                                         args.schedule)
+
+    # --- per-schedule sweep table and the gate of configs 2 and 3 (N = 1) -------------
+    sweep, gate = None, None
     if world == 1 and not args.no_sweep:
-        sweep = []
-        w_bench = dash.acc_split()
-        for s, g in probs:
-            row = {"seqlen": s[1], "batch": s[0], "heads": s[2], "acc_split": dash.acc_split(s[1]),
-                   "auto": dash.resolve_schedule(s, causal, "auto")}
-            f = fa_flops(*s, causal)
-            cases = [("naive", "naive", True, w_bench), ("descending", "descending", True, w_bench),
-                     ("shift", "shift", True, w_bench), ("atomic", "naive", False, w_bench)]
-            if dash.acc_split(s[1]) != 1:
-                cases += [("naive_w1", "naive", True, 1), ("descending_w1", "descending", True, 1),
-                          ("shift_w1", "shift", True, 1)]
-            # Round-robin over the cases, SWEEP_ROUNDS times, median per case:
-            # every schedule sees the same clock / power history (a case timed
-            # right after a cool-down would otherwise be favoured).
-            times = {name: [] for name, *_ in cases}
-            nst = max(3, args.steps)
-            for _ in range(SWEEP_ROUNDS):
-                for name, sched, det, w in cases:
-                    if row.get(name + "_error"):
-                        continue
-                    dash.set_acc_split(w)
-                    try:
-                        times[name].append(time_steps(
-                            torch, lambda: run_bwd(dash, g, causal, sched, det), nst, 2, 1))
-                    except dash.DashError as e:
-                        row[name + "_error"] = str(e)
-            for name, *_ in cases:
-                row[name] = (f * nst / (statistics.median(times[name]) / 1e3) / 1e12
-                             if times[name] and not row.get(name + "_error") else None)
-            row["rounds"] = SWEEP_ROUNDS
-            dash.set_acc_split(w_bench)
-            for suffix in ("", "_w1"):
-                if row.get("naive" + suffix) is None:
-                    continue
-                best = max(v for v in (row.get("descending" + suffix), row.get("shift" + suffix))
-                           if v is not None)
-                gap = row["atomic"] - row["naive" + suffix]
-                row["best_dash" + suffix] = best
-                # AMB-19: a gap below 2 % of the atomic variant (or a negative one:
-                # NAIVE already at or above it) -> pass iff within 2 % of NAIVE
-                if gap < 0.02 * row["atomic"]:
-                    row["gap_closed" + suffix] = None
-                    row["pass" + suffix] = best >= 0.98 * row["naive" + suffix]
-                else:
-                    row["gap_closed" + suffix] = (best - row["naive" + suffix]) / gap
-                    row["pass" + suffix] = row["gap_closed" + suffix] >= 0.5
-            # Against the paper's own baseline: FA3-style NAIVE with one ordered
-            # accumulator per dQ tile (W = 1), DASH schedules at
-            # the library's W (AMB-27 is part of this build's ordered reduction).
-            if row.get("naive_w1") is not None and row.get("best_dash") is not None:
-                gap = row["atomic"] - row["naive_w1"]
-                row["gap_closed_vs_fa3_naive"] = ((row["best_dash"] - row["naive_w1"]) / gap
-                                                  if gap >= 0.02 * row["atomic"] else None)
-                row["pass_vs_fa3_naive"] = (row["gap_closed_vs_fa3_naive"] >= 0.5
-                                            if row["gap_closed_vs_fa3_naive"] is not None
-                                            else row["best_dash"] >= 0.98 * row["naive_w1"])
-            sweep.append(row)
+        sweep = sweep_rows(dash, torch, probs, causal, args.steps)
+        gate = {f"{'causal' if causal else 'full'}_hd{d}": gate_summary(sweep)}
+        if not args.no_gate:
+            del probs
+            torch.cuda.empty_cache()
+            others = [(c, hd) for c, hd in ((True, 128), (False, 128), (False, 64), (True, 64))
+                      if (c, hd) != (causal, d)]
+            for c, hd in others:
+                ps = [(s, make_problem(*s, c, 0, 1, "strong", dash, torch)) for s in shapes(hd, seqlens)]
+                rows = sweep_rows(dash, torch, ps, c, args.steps)
+                gate[f"{'causal' if c else 'full'}_hd{hd}"] = dict(gate_summary(rows), rows=rows)
+                del ps
+                torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -521,18 +653,21 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": args.scaling,
+            "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded N(0,1) bf16 q,k,v,dO; O, L from dash_attn_fwd)",
             "config": dict(workload_config(args, world),
                            schedule_resolved={str(sh[1]): dash.resolve_schedule(sh, causal, args.schedule)
-                                              for sh, _ in probs},
-                           acc_split_resolved={str(sh[1]): dash.acc_split(sh[1]) for sh, _ in probs}),
-            "frac_of_peak": value / peak,
+                                              for sh in full_shapes},
+                           acc_split_resolved={str(sh[1]): dash.acc_split(sh[1]) for sh in full_shapes}),
+            "frac_of_peak": value / peak / world,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": dash.bwd_launches(causal, args.schedule, True) * len(probs) * args.steps,
+            "gpu_launches": dash.bwd_launches(causal, args.schedule, True) * len(full_shapes) * args.steps,
             "clocks": clk.summary(),
+            "sharding_bitwise_identical": sharding_ok,
+            "gate": gate,
             "sweep": sweep,
         }
         print(json.dumps(line), flush=True)

@@ -87,12 +87,15 @@ typedef struct {
 dash_status dash_attn_fwd(const dash_shape* shape, const void* q, const void* k, const void* v,
                           void* o, float* lse, int causal, void* stream);
 
-/* Bytes of device workspace dash_attn_bwd needs for this problem: room for
- * the largest W = 8 interleaved fp32 dQ accumulators [8][B,H,N,d] (Alg.1
- * line 34's "dQ_i in global memory"; AMB-27),
- * D = rowsum(dO o O) fp32 [B,H,N] (Alg.1 line 1; AMB-2), one int32
- * ticket per (W, b, h, Q sub-tile) (the "global order"), the job
- * counter and the schedule table.  Returns 0 for an invalid shape. */
+/* Bytes of device workspace dash_attn_bwd needs for this problem: the W
+ * interleaved fp32 dQ accumulators [W][B,H,N,d] (Alg.1 line 34's "dQ_i in
+ * global memory"; AMB-27) -- W = dash_attn_bwd_acc_split(N) under the
+ * current setting when deterministic != 0, W = 1 for the atomic variant --
+ * D = rowsum(dO o O) and -L*log2(e) fp32 [B,H,N] (Alg.1 line 1, P:355;
+ * AMB-2), one int32 ticket per (accumulator, b, h, Q sub-tile) (the "global
+ * order"), the job counter and the error flag.  The accumulators
+ * sit at offset 0.  Returns 0 for an invalid shape.  A workspace sized under
+ * one W setting is rejected (DASH_ERR_WORKSPACE) by a call that needs more. */
 size_t dash_attn_bwd_workspace_bytes(const dash_shape* shape, int causal, int schedule,
                                      int deterministic);
 
@@ -144,9 +147,11 @@ dash_status dash_attn_bwd_host(const dash_shape* shape, const void* q, const voi
                                int deterministic, void* workspace, size_t workspace_bytes,
                                void* stream);
 
-/* Synchronises `stream` and reports DASH_ERR_DEADLOCK if any ticket wait in
- * an earlier dash_attn_bwd on this workspace exceeded its spin bound (the
- * kernel then abandons the ordered add; outputs are invalid), else DASH_OK. */
+/* Synchronises `stream` and reports DASH_ERR_DEADLOCK if a ticket wait of
+ * the most recent dash_attn_bwd on this workspace exceeded its bound (see
+ * dash_attn_bwd_set_watchdog): the kernel then raises a device-wide abort
+ * flag, every warp role leaves, and the outputs are invalid.  Else DASH_OK.
+ * Every dash_attn_bwd resets the flag at its start. */
 dash_status dash_check_workspace(const dash_shape* shape, int causal, int schedule,
                                  int deterministic, const void* workspace, void* stream);
 
@@ -217,7 +222,7 @@ int dash_attn_bwd_resolve_schedule(const dash_shape* shape, int causal, int sche
 
 /* Number W of interleaved fp32 dQ accumulators the deterministic backward
  * uses (AMB-27).  W = 1 is the paper's single global order per dQ tile
- * (P:395-397).  W = 2 or 4: the contribution of rank k is added, in rank
+ * (P:395-397).  W in {2, 4, 8}: the contribution of rank k is added, in rank
  * order, into accumulator k mod W under that accumulator's own ticket, and
  * the convert kernel sums the accumulators in index order -- a fixed order,
  * so results stay bitwise deterministic, while consecutive adds into one
@@ -249,6 +254,18 @@ dash_status dash_attn_bwd_dump(const dash_shape* shape, const void* q, const voi
                                void* dq, void* dk, void* dv, int causal, int schedule,
                                int deterministic, void* workspace, size_t workspace_bytes,
                                float* partials, size_t partial_bytes, void* stream);
+
+/* Bound of one ticket wait of the ordered reduction, in SM clock cycles
+ * (clock64); 0 restores the default (2^36, ~35 s at 1.965 GHz).  A wait that
+ * exceeds it aborts the launch (dash_check_workspace -> DASH_ERR_DEADLOCK)
+ * instead of hanging the GPU.  Host-global; DASH_ERR_INVALID_ARG if < 0. */
+dash_status dash_attn_bwd_set_watchdog(long long cycles);
+
+/* Verification only (the watchdog test): the next dash_attn_bwd issued by the
+ * calling thread presets its first ticket to `poison` (0 = no fault) -- a
+ * rank no ordered add ever reaches -- so a wait can only end through the
+ * watchdog.  Always DASH_OK. */
+dash_status dash_attn_bwd_inject_fault(int poison);
 
 /* Number of device kernel launches one dash_attn_bwd makes (for accounting):
  * 3 (preprocess, main, dQ convert). */

@@ -248,24 +248,3 @@ def longest_path(n_nodes: int, edges: list, source: int, sink: int) -> int:
     if seen != n_nodes:
         raise ValueError("graph has a cycle")
     return dist[sink]
-
-
-def closed_form(schedule: int, n: int, mask: int, m: int, c: int, r: int):
-    """The paper's closed forms, as read in SURVEY.md §8(c) c4 (AMB-8/9/10).
-
-    Returns None where the paper states no form.  These are what the tests
-    compare simulate() against -- they are pins, not part of simulate().
-    """
-    if schedule == NAIVE:
-        return m * n * (c + r) + (n - 1) * r                      # P:87, P:89 (AMB-8)
-    if schedule == DESCENDING and mask == FULL:
-        return m * n * (c + r) + (n - 1) * r                      # derived: same chain as naive
-    if schedule == DESCENDING and mask == CAUSAL:
-        if m % 2 == 0:
-            return m * (n + 1) * (c + r) // 2 + (n - 1) * r       # P:103 (AMB-9)
-        return (m - 1) * (n + 1) * (c + r) // 2 + n * (c + r)     # AMB-9, odd m (derived)
-    if schedule == SHIFT and mask == FULL:
-        return m * n * (c + r)                                    # P:141
-    if schedule == SHIFT and mask == CAUSAL:
-        return ((m + 1) // 2) * (n + 1) * (c + r)                 # P:141 (AMB-10 for odd m)
-    return None

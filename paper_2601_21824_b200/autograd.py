@@ -3,8 +3,10 @@ deterministic)` with forward = dash_attn_fwd and backward = dash_attn_bwd.
 
 Marshalling only (every step runs in libdash.so kernels): tensors are
 bf16 [B, N, H, d] CUDA tensors (the layout a fused QKV projection produces
-with .view(B, N, H, d)); the backward's workspace is cached per (shape,
-device) so a training loop does not reallocate it every step.  The
+with .view(B, N, H, d)); the backward's workspace is cached for the last
+few (shape, device, size) keys (an LRU of _WS_CACHE_MAX entries) so a
+training loop does not reallocate it every step and variable sequence
+lengths do not grow GPU memory without bound.  The
 deterministic backward is bitwise reproducible (Algorithm 1, PAPER.md
 P:351-397); `deterministic=False` selects the atomic comparison variant.
 """
@@ -12,17 +14,23 @@ from __future__ import annotations
 
 import torch
 
+from collections import OrderedDict
+
 from . import dash
 
-_ws_cache: dict = {}
+_WS_CACHE_MAX = 4
+_ws_cache: "OrderedDict[tuple, torch.Tensor]" = OrderedDict()
 
 
-def _workspace(shape, causal, device):
-    key = (tuple(shape), bool(causal), str(device))
-    ws = _ws_cache.get(key)
+def _workspace(shape, causal, deterministic, device):
+    nbytes = dash.workspace_bytes(shape, causal, dash.NAIVE, deterministic)
+    key = (tuple(shape), bool(causal), str(device), nbytes)
+    ws = _ws_cache.pop(key, None)
     if ws is None:
-        ws = dash.alloc_workspace(shape, causal, dash.NAIVE, True, device)
-        _ws_cache[key] = ws
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    _ws_cache[key] = ws  # most recently used last
+    while len(_ws_cache) > _WS_CACHE_MAX:
+        _ws_cache.popitem(last=False)
     return ws
 
 
@@ -38,7 +46,7 @@ class DashAttention(torch.autograd.Function):
     @staticmethod
     def backward(ctx, do):
         q, k, v, o, lse = ctx.saved_tensors
-        ws = _workspace(q.shape, ctx.causal, q.device)
+        ws = _workspace(q.shape, ctx.causal, ctx.deterministic, q.device)
         dq, dk, dv = dash.attn_bwd(q, k, v, o, do.contiguous(), lse, ctx.causal, ctx.schedule,
                                    ctx.deterministic, workspace=ws)
         return dq, dk, dv, None, None, None

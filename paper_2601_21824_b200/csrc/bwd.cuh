@@ -56,16 +56,15 @@ struct BwdArgs {
   int deterministic;
   unsigned long long* trace;  // optional clock64 trace [grid][trace_cap][16] (measurement only)
   int trace_cap;
-  int debug;  // timing experiments only (env DASH_DEBUG): bit 0 skips the dQ reduce ops,
-             // bit 2 skips the dQ staging (with bit 0: the compute pipeline alone)
+  long long spin_bound;  // ticket-wait watchdog, clock64 cycles (dash_attn_bwd_set_watchdog)
   float* dump;  // verification only: every dQ partial, [B*H][N/128][N][d] fp32
-  // Interleaved accumulation (AMB-27): split = W in {1, 2, 4}.  The contribution
+  // Interleaved accumulation (AMB-27): split = W in {1, 2, 4, 8}.  The contribution
   // of rank k goes into accumulator k % W (dQacc + (k % W) * B*H*N*d) in the
   // order of its ticket set k % W (value k / W); the convert kernel adds the W
   // accumulators in index order.  W = 1 is the paper's single global order.
   int split;
   int n_tickets;  // tickets per accumulator
-  float* dqacc;   // the accumulators (1-D bulk reduce variant, V = 3)
+  float* dqacc;   // the W accumulators [W][B,H,N,d] fp32 (1-D bulk reduce at d = 128)
   // Early claim of the next job (see the producer): 0 = claim only after every
   // ordered add of the current job is released; 1 = the producer claims the next
   // job as soon as it has issued the current job's last load, when that is
@@ -90,71 +89,47 @@ struct BwdArgs {
           clock64();                                                                      \
   } while (0)
 
-// V selects the smem split between the Q/dO ring and the dQ staging:
-// V = 0: NSTAGE-deep ring (3 at d = 128), one staging buffer of a whole
-//        sub-tile's partial (one ticket per sub-tile);
-// V = 1: one staging buffer per reducer (the drain can stage the next partial
-//        while the previous one still waits for its ticket), ring of 2;
-// V = 2: the partial staged and reduced in two halves of BR/2 rows, each with
-//        its own ticket (two shorter hand-offs per sub-tile), one half-size
-//        buffer per reducer, same ring as V = 0;
-// V = 3: as V = 0, but d = 128 partials are staged row-major (linear) and
-//        reduced with 1-D bulk copies (cp.reduce.async.bulk, no tensor map):
-//        a sub-tile's partial is one contiguous 32 KB run of dQacc.  The
-//        buffer is a ring of two halves (rows 0-31, 32-63): the drain writes
-//        one half while the bulk engine still reads the other;
-// V = 4: as V = 3 with a ring of four quarters (16 rows, 8 KB each): a
-//        quarter is refilled as soon as the bulk engine has read it, so
-//        staging the next partial overlaps reading the previous one;
-// V = 5: as V = 3 with a ring of THREE half-unit slots (48 KB: 1.5 partials
-//        of staging capacity), paid for by a single dS^T smem buffer (the
-//        softmax then waits for dQ of the previous sub-tile before writing
-//        dS^T);
-// V = 6: split reduction (d = 128): rows 0-31 of a partial are staged and
-//        reduced by the bulk engine (1-D, ring of two 16 KB slots), rows 32-63
-//        are added by the drain warps straight from registers with
-//        red.global.add.f32 (st.global for the first contribution) once the
-//        agent has acquired the ticket -- the two halves travel to L2 in
-//        parallel.  The agent releases the ticket after its bulk writes have
-//        completed and every drain thread has arrived (release.cta) after its
-//        red ops, so the ticket's st.release.gpu is cumulative over both.
-template <int D, int V = 0>
+// Shared-memory plan.  The fp32 dQ partial of a sub-tile (32 KB at both head
+// dims) is staged once and handed to the bulk engine:
+//   d = 128 (LINEAR): staged row-major and reduced with 1-D bulk copies
+//     (cp.reduce.async.bulk, no tensor map) -- a sub-tile's partial is one
+//     contiguous 32 KB run of dQacc.  The buffer is a ring of two halves (rows
+//     0-31, 32-63): the drain writes one half while the bulk engine still
+//     reads the other.
+//   d = 64: staged as SW128 boxes of 32 fp32 columns and reduced with 2-D
+//     tensor-map bulk reduces (a 128-row unit is not one contiguous run).
+// Measured alternatives (round 1, profiles/r01_experiments/): one staging
+// buffer per reducer with a 2-stage ring, half-size units with their own
+// tickets, a 4-part or 3-slot ring, and half bulk / half red.global were all
+// neutral or slower; they are no longer built.
+template <int D>
 struct BwdCfg {
   static constexpr int NTHREADS = 512;
   static constexpr int BC = 128;                    // KV tile rows (TMEM lanes)
   static constexpr int BR = (D == 128) ? 64 : 128;  // Q sub-tile rows
   static constexpr int NSUB = 128 / BR;             // sub-tiles per schedule Q tile
-  static constexpr int NSTAGE = (D == 128 && V != 1) ? 3 : 2;  // Q/dO/L/D ring depth
-  static constexpr int NSTG = (V == 1 || V == 2) ? 2 : 1;     // dQ staging buffers
-  static constexpr bool LINEAR = (V == 3 || V == 4 || V == 5) && D == 128;  // 1-D bulk reduce
-  static constexpr bool SPLITRED = (V == 6 && D == 128);  // half bulk, half red.global
-  static constexpr int NPART = (V == 4) ? 4 : 2;  // linear staging: parts per partial
-  static constexpr int RING = (V == 5) ? 3 : NPART;  // linear staging: part slots in the ring
+  static constexpr int NSTAGE = (D == 128) ? 3 : 2; // Q/dO/L/D ring depth
+  static constexpr bool LINEAR = (D == 128);        // 1-D bulk reduce of a row-major partial
+  static constexpr int NPART = 2;                   // linear staging: parts (= ring slots)
   static constexpr int NSMX = 2;                    // softmax warpgroups (column halves)
   static constexpr int SMX_COLS = BR / NSMX;        // columns per softmax thread
   static constexpr uint32_t KV_BYTES = BC * D * 2;
   static constexpr uint32_t Q_BYTES = BR * D * 2;
   static constexpr uint32_t P_BYTES = BC * BR * 2;
-  // The fp32 dQ partial of a sub-tile is staged and reduced in units of
-  // STG_ROWS rows, each with its own ticket.  (Measured: splitting the d = 128
-  // partial into 32-row halves to afford a 4-stage Q/dO ring with one dS^T
-  // buffer was slower -- the softmax then waits on the dQ MMA.)
-  static constexpr int STG_ROWS = V == 2 ? BR / 2 : BR;
-  static constexpr int NUNIT = BR / STG_ROWS;  // staging units per sub-tile
+  // One staging unit (and one ticket) per Q sub-tile.
+  static constexpr int STG_ROWS = BR;
   static constexpr uint32_t DQ_BYTES = STG_ROWS * D * 4;
   static constexpr uint32_t OFF_K = 0;
   static constexpr uint32_t OFF_V = OFF_K + KV_BYTES;
   static constexpr uint32_t OFF_Q = OFF_V + KV_BYTES;            // NSTAGE stages
   static constexpr uint32_t OFF_DO = OFF_Q + NSTAGE * Q_BYTES;   // NSTAGE stages
-  static constexpr int NDS = (V == 5 && D == 128) ? 1 : 2;       // dS^T smem buffers
-  static constexpr int NPT = 1;                                  // P^T TMEM buffers
+  static constexpr int NDS = 2;                                  // dS^T smem buffers
   // d = 128: dS^T also lives in TMEM so dK += dS^T Q runs as a TS MMA (A from
   // TMEM, full rate, no smem read); d = 64 has no TMEM room left for it.
   static constexpr bool DS_IN_TMEM = (D == 128);
   static constexpr uint32_t OFF_DS = OFF_DO + NSTAGE * Q_BYTES;  // NDS x dS^T bf16 SW128
-  static constexpr uint32_t OFF_DQ = OFF_DS + NDS * P_BYTES;     // fp32 SW128 staging buffer
-  static constexpr uint32_t STG_BYTES =
-      LINEAR ? RING * (DQ_BYTES / NPART) : SPLITRED ? DQ_BYTES : NSTG * DQ_BYTES;
+  static constexpr uint32_t OFF_DQ = OFF_DS + NDS * P_BYTES;     // fp32 staging buffer
+  static constexpr uint32_t STG_BYTES = DQ_BYTES;
   static constexpr uint32_t OFF_L = OFF_DQ + STG_BYTES;           // NSTAGE x BR floats
   static constexpr uint32_t OFF_DV = OFF_L + NSTAGE * BR * 4;    // NSTAGE x BR floats
   static constexpr uint32_t OFF_BAR = OFF_DV + NSTAGE * BR * 4;
@@ -173,7 +148,7 @@ struct BwdCfg {
   static constexpr uint32_t T_DQ = 2 * BR + 2 * D;  // 64 columns
   static constexpr uint32_t T_PT = T_DQ + 64;       // BR/2 columns of packed bf16 P^T
   static constexpr uint32_t T_DST = T_PT + BR / 2;  // BR/2 columns of packed bf16 dS^T (d = 128)
-  static_assert(T_PT + NPT * BR / 2 + (DS_IN_TMEM ? BR / 2 : 0) == 512, "TMEM budget");
+  static_assert(T_PT + BR / 2 + (DS_IN_TMEM ? BR / 2 : 0) == 512, "TMEM budget");
   static_assert(SMEM_BYTES <= 232448, "smem budget");
   static_assert(SMX_COLS % 32 == 0, "softmax column split");
 };
@@ -185,20 +160,18 @@ enum : int {
   B_S_FULL = 4, B_S_EMPTY = 5,         // S^T/dP^T in TMEM (commit) / read by softmax (256)
   B_P_FULL = 6,                        // P^T (TMEM) and dS^T (smem) written (256)
   B_DQ_FULL = 7, B_DQ_EMPTY = 8,       // dQ partial in TMEM (commit) / drained (128)
-  B_PT_EMPTY0 = 9,                     // P^T TMEM buffer consumed by dV (commit)
+  B_PT_EMPTY = 9,                      // P^T TMEM buffer consumed by dV (commit)
   B_DST_EMPTY = 10,                    // dS^T TMEM buffer consumed by dK (commit)
-  B_STG_EMPTY1 = 11,                   // staging buffer 1 read by the reduce (1), NSTG = 2
-  B_DS_EMPTY0 = 22, B_DS_EMPTY1 = 23,  // dS^T smem buffer consumed by dK, dQ (commit)
+  B_STG_EMPTY1 = 11,                   // linear staging part 1 read by the reduce (1)
   B_ACC_FULL = 12, B_ACC_EMPTY = 13,   // dK/dV complete (commit) / drained (256)
-  B_STG_EMPTY = 14,                    // staging (buffer 0) read by the reduce (1)
+  B_STG_EMPTY = 14,                    // staging (part 0) read by the reduce (1)
   B_JOB_DONE = 15,                     // every reducer agent released the job (NAG)
+  B_MMA_DRAIN = 16,                    // exit: every issued MMA has completed (commit)
   B_Q_FULL0 = 18,                      // + stage (<= 4): Q/dO/L/D loaded (tx)
-  B_Q_EMPTY0 = 26,                     // + stage (<= 4): stage consumed (commit)
-  B_STG_EMPTY2 = 16, B_STG_EMPTY3 = 17, // linear staging parts 2, 3 read (1), V = 4
+  B_DS_EMPTY0 = 22, B_DS_EMPTY1 = 23,  // dS^T smem buffer consumed by dK, dQ (commit)
   B_PF0 = 24,                          // + (t - 1) % 2: producer's claim decision for job t (1)
+  B_Q_EMPTY0 = 26,                     // + stage (<= 4): stage consumed (commit)
   B_SLOT_FREE0 = 30,                   // + j % 2: every warp has read job j's slot (16)
-  B_TKT0 = 36,                         // + agent: ticket of the agent's unit acquired (1), V = 6
-  B_RDONE0 = 38,                       // + agent: drain's direct half added (128), V = 6
   B_AGF0 = 32,                         // + h * NAG + agent: staging (part h) written for
                                        // the agent of unit x (x % NAG) (128)
   B_COUNT = 40
@@ -261,23 +234,20 @@ __device__ __forceinline__ TaskView decode_task(const BwdArgs& a, const JobView&
   return v;
 }
 
-template <int D, int V>
+template <int D>
 __global__ void __launch_bounds__(512, 1)
     dash_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_dqacc, const BwdArgs args) {
-  using C = BwdCfg<D, V>;
-  constexpr int BR = C::BR, NSUB = C::NSUB, NSTAGE = C::NSTAGE, NSTG = C::NSTG;
+  using C = BwdCfg<D>;
+  constexpr int BR = C::BR, NSUB = C::NSUB, NSTAGE = C::NSTAGE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t pad = (1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023;
   if (pad > C::SLACK) __trap();
   uint8_t* smem = smem_raw + pad;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  auto stg_empty = [&](uint32_t unit) { return &bars[(unit % NSTG) ? B_STG_EMPTY1 : B_STG_EMPTY]; };
   // linear staging: barrier "part hh of the buffer has been read by the bulk engine"
-  auto part_empty = [&](int hh) {
-    return &bars[hh == 0 ? B_STG_EMPTY : hh == 1 ? B_STG_EMPTY1 : hh == 2 ? B_STG_EMPTY2 : B_STG_EMPTY3];
-  };
+  auto part_empty = [&](int hh) { return &bars[hh == 0 ? B_STG_EMPTY : B_STG_EMPTY1]; };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_MISC);
   int* job_slot = reinterpret_cast<int*>(smem + C::OFF_MISC + 8);  // [2]
   volatile int* claim_mode = reinterpret_cast<volatile int*>(smem + C::OFF_MISC + 16);  // [2]
@@ -305,8 +275,6 @@ __global__ void __launch_bounds__(512, 1)
     for (int i = 0; i < C::NPART * NAG; ++i) ptx::mbar_init(&bars[B_AGF0 + i], 128);
     ptx::mbar_init(&bars[B_JOB_DONE], NAG);
     ptx::mbar_init(&bars[B_SLOT_FREE0], 16);
-    if constexpr (C::SPLITRED)
-      for (int i = 0; i < NAG; ++i) ptx::mbar_init(&bars[B_RDONE0 + i], 128);
     ptx::mbar_init(&bars[B_SLOT_FREE0 + 1], 16);
     ptx::fence_mbar_init();
     ptx::fence_async_smem();
@@ -314,7 +282,7 @@ __global__ void __launch_bounds__(512, 1)
     ptx::prefetch_tmap(&tm_k);
     ptx::prefetch_tmap(&tm_v);
     ptx::prefetch_tmap(&tm_do);
-    ptx::prefetch_tmap(&tm_dqacc);
+    if constexpr (!C::LINEAR) ptx::prefetch_tmap(&tm_dqacc);
   }
   if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
@@ -389,7 +357,11 @@ __global__ void __launch_bounds__(512, 1)
         if (lane == 0) {
           int mode = 2;
           wait_slot_free(it_job);  // slot it_job % 2 / claim_mode slot reusable
-          if (args.prefetch && !args.cyclic) {
+          if (ptx::aborted()) {
+            // watchdog tripped: publish the terminal job so every role leaves
+            job_slot[it_job & 1] = args.total_jobs;
+            mode = 1;
+          } else if (args.prefetch && !args.cyclic) {
             job_slot[it_job & 1] = atomicAdd(args.job_counter, 1);
             mode = 1;
           } else if (args.prefetch) {
@@ -412,13 +384,20 @@ __global__ void __launch_bounds__(512, 1)
         }
         __syncwarp();
       }
+      // Exit: no TMA write may still be in flight when the CTA retires (matters
+      // only after a watchdog abort, when consumers stop waiting for loads).
+      if (q_cnt > 0) {
+        for (uint32_t k = (q_cnt > NSTAGE ? q_cnt - NSTAGE : 0); k < q_cnt; ++k)
+          ptx::mbar_wait_bounded(&bars[B_Q_FULL0 + k % NSTAGE], (k / NSTAGE) & 1);
+      }
+      if (kv_cnt > 0) ptx::mbar_wait_bounded(&bars[B_KV_FULL], (kv_cnt - 1) & 1);
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ==============================
     {  // whole warp converged; elect.sync issues (keeps descriptors uniform)
       uint32_t it_job = 0, kv_cnt = 0, x = 0, acc_cnt = 0;
       // Base descriptors of every smem operand, built once; per-stage/buffer
-      // variants differ by a constant offset (in 16-B units) added per use.
+      // copies differ by a constant offset (in 16-B units) added per use.
       const uint32_t s0 = ptx::smem_u32(smem);
       const uint64_t dK_k = tile_desc<false>(s0 + C::OFF_K, 128);   // K as K-major A
       const uint64_t dK_mn = tile_desc<true>(s0 + C::OFF_K, 128);   // K as MN-major A/B
@@ -467,15 +446,15 @@ __global__ void __launch_bounds__(512, 1)
             // S/dP of the next sub-tile go into the tensor pipe while the
             // softmax warps turn this one into P^T / dS^T.
             if (u + 1 < nsub) issue_sdp(xx + 1);
-            const uint32_t st = xx % NSTAGE, sb = xx % C::NDS, pb = xx % C::NPT;
+            const uint32_t st = xx % NSTAGE, sb = xx % C::NDS;
             ptx::mbar_wait_u(&bars[B_P_FULL], xx & 1);
             if (lane == 0) DASH_TRACE_MARK(1, xx);
             if (u == 0 && acc_cnt > 0) ptx::mbar_wait_u(&bars[B_ACC_EMPTY], (acc_cnt - 1) & 1);
             ptx::tc_fence_after();
             // dV += P^T dO  (A = P^T straight from TMEM)   (Alg.1 line 25)
-            umma_gemm_ts_d<D, BR, true, BR>(tbase + C::T_DV, tbase + C::T_PT + pb * (BR / 2),
-                                            ddO_mn + st * Q_STEP, u > 0);
-            ptx::mma_commit_e(&bars[B_PT_EMPTY0 + pb]);
+            umma_gemm_ts_d<D, BR, true, BR>(tbase + C::T_DV, tbase + C::T_PT, ddO_mn + st * Q_STEP,
+                                            u > 0);
+            ptx::mma_commit_e(&bars[B_PT_EMPTY]);
             // dK += dS^T Q   (Alg.1 line 26)
             if constexpr (C::DS_IN_TMEM) {
               umma_gemm_ts_d<D, BR, true, BR>(tbase + C::T_DK, tbase + C::T_DST, dQ_mn + st * Q_STEP,
@@ -509,6 +488,9 @@ __global__ void __launch_bounds__(512, 1)
           ts = te;
         }
       }
+      // Exit: every issued MMA has completed before TMEM is released.
+      ptx::mma_commit_e(&bars[B_MMA_DRAIN]);
+      ptx::mbar_wait_bounded(&bars[B_MMA_DRAIN], 0);
     }
   } else if (warp == 2 || warp == 3) {
     // ======================== ordered dQ reducers ==========================
@@ -529,16 +511,15 @@ __global__ void __launch_bounds__(512, 1)
         ptx::mbar_wait(&bars[B_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
         const int g = job_slot[it_job & 1];
         slot_read(it_job);
-        if (g >= args.total_jobs) break;
+        if (g >= args.total_jobs || ptx::aborted()) break;
         const JobView jv = decode_job(args, g);
         for (int t = jv.t0; t < jv.t1; ++t) {
           const TaskView tv = decode_task(args, jv, args.tasks[t]);
           const int q = tv.q, rank = tv.rank;
-          for (int sub = 0; sub < NSUB; ++sub) {
-           for (int h = 0; h < C::NUNIT; ++h, ++x) {  // x counts staging units here
+          for (int sub = 0; sub < NSUB; ++sub, ++x) {  // x counts staging units (= sub-tiles)
             if ((x % NAG) != agent) continue;
             const uint32_t ph = (x / NAG) & 1;  // this agent's phase on its FULL barriers
-            const int urow = q * 128 + sub * BR + h * C::STG_ROWS;  // first Q row of the unit
+            const int urow = q * 128 + sub * BR;  // first Q row of the unit
             const int par = rank % args.split, rank_w = rank / args.split;  // AMB-27
             int* ticket = args.tickets + static_cast<size_t>(par) * args.n_tickets +
                           static_cast<size_t>(tv.bh) * n_units + urow / C::STG_ROWS;
@@ -552,8 +533,7 @@ __global__ void __launch_bounds__(512, 1)
                 while (ptx::ld_relaxed(ticket) != rank_w) {
                   __nanosleep(32);
                   if ((++polls & ptx::kAbortPollMask) != 0) continue;  // no extra round trip per poll
-                  if (clock64() - t_start > 8 * ptx::kWatchdogCycles ||
-                      *reinterpret_cast<volatile int*>(&ptx::g_dash_abort)) {  // ~35 s bound
+                  if (clock64() - t_start > args.spin_bound || ptx::aborted()) {
                     atomicExch(args.error_flag, 1);
                     atomicExch(&ptx::g_dash_abort, 1);
                     break;
@@ -564,60 +544,37 @@ __global__ void __launch_bounds__(512, 1)
               // Order the ticket acquire (generic proxy) before the reduce (async proxy).
               ptx::fence_async_global();
             }
-            if (h == 0) DASH_TRACE_MARK(7, x / C::NUNIT);
+            DASH_TRACE_MARK(7, x);
             // Add dQ_local to dQ (Alg.1 line 34); rank 0 stores (no zero-fill needed).
             // row of dQacc [W][B*H*N, D]
             const int grow = (par * args.B * args.H + tv.bh) * args.N + urow;
-            const uint8_t* stg = smem + C::OFF_DQ + (x % NSTG) * C::DQ_BYTES;
-            if constexpr (C::SPLITRED) {
-              // the drain may now add rows 32-63 itself (ordered after this acquire)
-              ptx::mbar_arrive(&bars[B_TKT0 + agent]);
-              constexpr uint32_t HB = C::DQ_BYTES / 2;
-              const uint32_t slot = x & 1;
-              ptx::mbar_wait(&bars[B_AGF0 + agent], ph);
-              if (h == 0) DASH_TRACE_MARK(13, x / C::NUNIT);
-              float* dst = args.dqacc + static_cast<size_t>(grow) * D;
-              const uint8_t* src = smem + C::OFF_DQ + slot * HB;
-              if (det && rank_w == 0) ptx::bulk_store(dst, src, HB);
-              else ptx::bulk_reduce_add_f32(dst, src, HB);
-              ptx::bulk_commit();
-              if (h == 0) DASH_TRACE_MARK(8, x / C::NUNIT);
-              ptx::bulk_wait_read<0>();
-              ptx::mbar_arrive(part_empty(slot));
-              // completion of both halves before the release: own bulk writes
-              // (wait_group below) and the drain's red ops (its arrive, release.cta)
-              ptx::mbar_wait(&bars[B_RDONE0 + agent], ph);
-            } else if constexpr (C::LINEAR) {
+            if constexpr (C::LINEAR) {
               // NPART parts, each reduced as soon as the drain has written it;
               // a part is handed back as soon as the bulk engine has read it
               float* dst0 = args.dqacc + static_cast<size_t>(grow) * D;
               constexpr uint32_t HB = C::DQ_BYTES / C::NPART;
-              (void)stg;
 #pragma unroll
               for (int hh = 0; hh < C::NPART; ++hh) {
-                const uint32_t slot = (x * C::NPART + hh) % C::RING;  // part slot in the ring
-                if (!(args.debug & 4)) ptx::mbar_wait(&bars[B_AGF0 + hh * NAG + agent], ph);
-                if (h == 0 && hh == C::NPART - 1) DASH_TRACE_MARK(13, x / C::NUNIT);  // all parts staged
-                if (!(args.debug & 1)) {
-                  float* dst = dst0 + hh * (HB / 4);
-                  const uint8_t* src = smem + C::OFF_DQ + slot * HB;
-                  if (det && rank_w == 0) ptx::bulk_store(dst, src, HB);
-                  else ptx::bulk_reduce_add_f32(dst, src, HB);
-                }
+                ptx::mbar_wait(&bars[B_AGF0 + hh * NAG + agent], ph);
+                if (hh == C::NPART - 1) DASH_TRACE_MARK(13, x);  // all parts staged
+                float* dst = dst0 + hh * (HB / 4);
+                const uint8_t* src = smem + C::OFF_DQ + hh * HB;
+                if (det && rank_w == 0) ptx::bulk_store(dst, src, HB);
+                else ptx::bulk_reduce_add_f32(dst, src, HB);
                 ptx::bulk_commit();
                 if (hh >= 1) {
                   ptx::bulk_wait_read<1>();  // part hh - 1 read: the drain may refill its slot
-                  ptx::mbar_arrive(part_empty((x * C::NPART + hh - 1) % C::RING));
+                  ptx::mbar_arrive(part_empty(hh - 1));
                 }
               }
-              if (h == 0) DASH_TRACE_MARK(8, x / C::NUNIT);
+              DASH_TRACE_MARK(8, x);
               ptx::bulk_wait_read<0>();
-              ptx::mbar_arrive(part_empty((x * C::NPART + C::NPART - 1) % C::RING));
+              ptx::mbar_arrive(part_empty(C::NPART - 1));
             } else {
-              if (!(args.debug & 4)) ptx::mbar_wait(&bars[B_AGF0 + agent], ph);
+              const uint8_t* stg = smem + C::OFF_DQ;
+              ptx::mbar_wait(&bars[B_AGF0 + agent], ph);
 #pragma unroll
               for (int blk = 0; blk < D / 32; ++blk) {
-                if (args.debug & 1) break;  // timing experiment: no reduce traffic
                 if (det && rank_w == 0) {
                   tma_store_2d(&tm_dqacc, stg + blk * C::STG_ROWS * 128, blk * 32, grow);
                 } else {
@@ -625,13 +582,13 @@ __global__ void __launch_bounds__(512, 1)
                 }
               }
               ptx::bulk_commit();
-              if (h == 0) DASH_TRACE_MARK(8, x / C::NUNIT);
+              DASH_TRACE_MARK(8, x);
               ptx::bulk_wait_read_all();  // staging may be overwritten from here on
-              ptx::mbar_arrive(stg_empty(x));
+              ptx::mbar_arrive(&bars[B_STG_EMPTY]);
             }
-            if (h == 0) DASH_TRACE_MARK(11, x / C::NUNIT);
+            DASH_TRACE_MARK(11, x);
             ptx::bulk_wait_all();
-            if (h == 0) DASH_TRACE_MARK(12, x / C::NUNIT);
+            DASH_TRACE_MARK(12, x);
             if (det) {
               // Advance the global order (Alg.1 line 35): proxy fence (the
               // reduce wrote through the async proxy) + gpu-scope release.
@@ -641,8 +598,7 @@ __global__ void __launch_bounds__(512, 1)
               ptx::fence_async_global();
               ptx::st_release(ticket, rank_w + 1);
             }
-            if (h == C::NUNIT - 1) DASH_TRACE_MARK(9, x / C::NUNIT);
-           }
+            DASH_TRACE_MARK(9, x);
           }
         }
         // Every agent has released every add of this job: only now may the
@@ -654,7 +610,8 @@ __global__ void __launch_bounds__(512, 1)
           ptx::mbar_wait(&bars[B_PF0 + (it_job & 1)], (it_job >> 1) & 1);
           if (claim_mode[it_job & 1] == 2) {
             wait_slot_free(it_job + 1);
-            job_slot[(it_job + 1) & 1] = atomicAdd(args.job_counter, 1);
+            job_slot[(it_job + 1) & 1] =
+                ptx::aborted() ? args.total_jobs : atomicAdd(args.job_counter, 1);
             ptx::mbar_arrive(&bars[B_JOB0 + ((it_job + 1) & 1)]);
           }
         }
@@ -676,7 +633,7 @@ __global__ void __launch_bounds__(512, 1)
       __syncwarp();
       if (lane == 0) slot_read(it_job);
       ++it_job;
-      if (g >= args.total_jobs) break;
+      if (g >= args.total_jobs || ptx::aborted()) break;
       const JobView jv = decode_job(args, g);
       // The next task's entry is loaded one task ahead: its L2 latency (~700
       // cycles) otherwise sits between two sub-tiles on the softmax's
@@ -688,7 +645,7 @@ __global__ void __launch_bounds__(512, 1)
         const int kv = tv.kv, q = tv.q;
         const bool diag = args.causal && (kv == q);
         for (int sub = 0; sub < NSUB; ++sub, ++x) {
-          const uint32_t st = x % NSTAGE, sb = x % C::NDS, pb = x % C::NPT;
+          const uint32_t st = x % NSTAGE, sb = x % C::NDS;
           uint8_t* pdS = smem + C::OFF_DS + sb * C::P_BYTES;
           ptx::mbar_wait(&bars[B_S_FULL], x & 1);
           ptx::mbar_wait(&bars[B_Q_FULL0 + st], (x / NSTAGE) & 1);
@@ -739,10 +696,9 @@ __global__ void __launch_bounds__(512, 1)
             };
             if (diag) smx(std::true_type{});
             else smx(std::false_type{});
-            // P^T -> TMEM buffer pb once dV of sub-tile x - NPT consumed it.
-            if (ch == 0 && x >= C::NPT)
-              ptx::mbar_wait(&bars[B_PT_EMPTY0 + pb], ((x / C::NPT) - 1) & 1);
-            ptx::tmem_st16(tbase + lane_off + C::T_PT + pb * (BR / 2) + cc0 / 2, pk);
+            // P^T -> TMEM once dV of sub-tile x - 1 consumed it.
+            if (ch == 0 && x >= 1) ptx::mbar_wait(&bars[B_PT_EMPTY], (x - 1) & 1);
+            ptx::tmem_st16(tbase + lane_off + C::T_PT + cc0 / 2, pk);
             if constexpr (C::DS_IN_TMEM) {
               // dS^T -> TMEM (A operand of the dK TS-MMA) once dK of x - 1 consumed it.
               if (ch == 0 && x >= 1) ptx::mbar_wait(&bars[B_DST_EMPTY], (x - 1) & 1);
@@ -801,7 +757,7 @@ __global__ void __launch_bounds__(512, 1)
       }
     }
   } else {
-    // ================== dQ drain: TMEM -> fp32 SW128 staging ==================
+    // ================== dQ drain: TMEM -> fp32 staging ==================
     const int tl = (warp & 3) * 32 + lane;  // TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     uint32_t it_job = 0, x = 0;
@@ -811,7 +767,7 @@ __global__ void __launch_bounds__(512, 1)
       __syncwarp();
       if (lane == 0) slot_read(it_job);
       ++it_job;
-      if (g >= args.total_jobs) break;
+      if (g >= args.total_jobs || ptx::aborted()) break;
       const JobView jv = decode_job(args, g);
       const int nx = (jv.t1 - jv.t0) * NSUB;
       for (int u = 0; u < nx; ++u, ++x) {
@@ -839,80 +795,30 @@ __global__ void __launch_bounds__(512, 1)
           }
         }
         uint8_t* stg0 = smem + C::OFF_DQ;
+        const uint32_t y = x;  // staging unit (one per sub-tile)
+        if constexpr (C::LINEAR) {
+          // row-major [STG_ROWS][128] fp32 in NPART parts; lane tl = d index, v[c] = Q row c
+          constexpr int HR = C::STG_ROWS / C::NPART;
 #pragma unroll
-        for (int h = 0; h < C::NUNIT; ++h) {
-          const uint32_t y = x * C::NUNIT + h;  // staging unit
-          if (args.debug & 4) continue;  // timing experiment: no staging (pure compute pipeline)
-          if constexpr (C::SPLITRED) {
-            // rows 0-31 -> bulk-engine staging slot y % 2; lane tl = d index, v[c] = Q row c
-            constexpr int HR = BR / 2;
-            const uint32_t slot = y & 1;
-            if (y >= 2) ptx::mbar_wait(part_empty(slot), ((y >> 1) - 1) & 1);
-            float* sdst = reinterpret_cast<float*>(stg0 + slot * (C::DQ_BYTES / 2));
+          for (int hh = 0; hh < C::NPART; ++hh) {
+            if (y >= 1) ptx::mbar_wait(part_empty(hh), (y - 1) & 1);
+            float* dst = reinterpret_cast<float*>(stg0 + hh * (C::DQ_BYTES / C::NPART));
 #pragma unroll
-            for (int c = 0; c < HR; ++c) sdst[c * 128 + tl] = v[c];
+            for (int c = hh * HR; c < (hh + 1) * HR; ++c) dst[(c - hh * HR) * 128 + tl] = v[c];
             ptx::fence_async_smem();
-            ptx::mbar_arrive(&bars[B_AGF0 + (y % NAG)]);
-            if (tl == 0) DASH_TRACE_MARK(6, x);
-            // rows 32-63 straight to dQacc once the unit's ticket is held
-            const TaskView tv = decode_task(args, jv, args.tasks[jv.t0 + u / NSUB]);
-            const int rank = tv.rank, par = rank % args.split;
-            const bool first = args.deterministic && rank / args.split == 0;
-            const size_t grow = static_cast<size_t>(par * args.B * args.H + tv.bh) * args.N +
-                                tv.q * 128 + (u % NSUB) * BR + HR;
-            float* gdst = args.dqacc + grow * D + tl;
-            ptx::mbar_wait(&bars[B_TKT0 + (y % NAG)], (y / NAG) & 1);
-            if (first) {
-#pragma unroll
-              for (int c = HR; c < BR; ++c) gdst[(c - HR) * D] = v[c];
-            } else {
-#pragma unroll
-              for (int c = HR; c < BR; ++c) ptx::red_add_f32(gdst + (c - HR) * D, v[c]);
-            }
-            ptx::mbar_arrive(&bars[B_RDONE0 + (y % NAG)]);
-            if (tl == 96) DASH_TRACE_MARK(14, x);
-            continue;
+            ptx::mbar_arrive(&bars[B_AGF0 + hh * NAG + (y % NAG)]);
           }
-          if constexpr (C::LINEAR) {
-            // row-major [STG_ROWS][128] fp32 in NPART parts; lane tl = d index, v[c] = Q row c
-            constexpr int HR = C::STG_ROWS / C::NPART;
+        } else {
+          if (y >= 1) ptx::mbar_wait(&bars[B_STG_EMPTY], (y - 1) & 1);
+          // Stage the partial as SW128 boxes of 32 fp32 columns:
+          // lane tl = Q row, v[c] = d column c.
+          const int r = tl;
 #pragma unroll
-            for (int hh = 0; hh < C::NPART; ++hh) {
-              const uint32_t k = y * C::NPART + hh, slot = k % C::RING;  // part slot in the ring
-              if (k >= C::RING) ptx::mbar_wait(part_empty(slot), ((k / C::RING) - 1) & 1);
-              float* dst = reinterpret_cast<float*>(stg0 + slot * (C::DQ_BYTES / C::NPART));
-#pragma unroll
-              for (int c = hh * HR; c < (hh + 1) * HR; ++c)
-                dst[(c - hh * HR) * 128 + tl] = v[h * C::STG_ROWS + c];
-              ptx::fence_async_smem();
-              ptx::mbar_arrive(&bars[B_AGF0 + hh * NAG + (y % NAG)]);
-            }
-            continue;
-          }
-          if (y >= NSTG) ptx::mbar_wait(stg_empty(y), ((y / NSTG) - 1) & 1);
-          uint8_t* stg = stg0 + (y % NSTG) * C::DQ_BYTES;
-          // Stage STG_ROWS rows of the fp32 partial as SW128 boxes of 32 columns.
-          if constexpr (D == 128) {
-            // lane tl = d index, v[c] = Q row c of the sub-tile
-            const int blk = tl >> 5, chunk = (tl & 31) >> 2, w = tl & 3;
-#pragma unroll
-            for (int c = 0; c < C::STG_ROWS; ++c) {
-              const uint32_t off =
-                  blk * C::STG_ROWS * 128 + c * 128 + ((chunk ^ (c & 7)) << 4) + w * 4;
-              *reinterpret_cast<float*>(stg + off) = v[h * C::STG_ROWS + c];
-            }
-          } else {
-            // lane tl = Q row, v[c] = d column c; unit h holds rows [h*STG_ROWS, +STG_ROWS)
-            const int r = tl - h * C::STG_ROWS;
-            if (r >= 0 && r < C::STG_ROWS) {
-#pragma unroll
-              for (int cc = 0; cc < 16; ++cc) {
-                const int blk = cc >> 3, chunk = cc & 7;
-                const uint32_t off = blk * C::STG_ROWS * 128 + r * 128 + ((chunk ^ (r & 7)) << 4);
-                *reinterpret_cast<float4*>(stg + off) =
-                    make_float4(v[cc * 4], v[cc * 4 + 1], v[cc * 4 + 2], v[cc * 4 + 3]);
-              }
-            }
+          for (int cc = 0; cc < 16; ++cc) {
+            const int blk = cc >> 3, chunk = cc & 7;
+            const uint32_t off = blk * C::STG_ROWS * 128 + r * 128 + ((chunk ^ (r & 7)) << 4);
+            *reinterpret_cast<float4*>(stg0 + off) =
+                make_float4(v[cc * 4], v[cc * 4 + 1], v[cc * 4 + 2], v[cc * 4 + 3]);
           }
           ptx::fence_async_smem();
           ptx::mbar_arrive(&bars[B_AGF0 + (y % NAG)]);
@@ -929,13 +835,13 @@ __global__ void __launch_bounds__(512, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tbase);
   }
-  if (tid == 0 && *reinterpret_cast<volatile int*>(&ptx::g_dash_abort)) atomicExch(args.error_flag, 2);
+  if (tid == 0 && ptx::aborted()) atomicExch(args.error_flag, 2);
 }
 
 // K1: D = rowsum(dO o O) (Alg.1 line 1; D in R^N per AMB-2), fp32 in a
 // fixed order, and lse2 = -L * log2(e) for the exp2 form of P = exp(S - L);
-// also resets tickets / job counter and (atomic variant only) zero-fills the
-// dQ accumulator.
+// also resets tickets / job counter / error flag and (atomic variant only)
+// zero-fills the dQ accumulator.
 template <int D>
 __global__ void dash_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
                                        const __nv_bfloat16* __restrict__ dout,
@@ -943,7 +849,7 @@ __global__ void dash_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
                                        float* __restrict__ lse2, int B, int N, int H,
                                        int* __restrict__ zero_i32, int n_zero_i32,
                                        float4* __restrict__ zero_f32, size_t n_zero_f4,
-                                       int* __restrict__ job_counter) {
+                                       int* __restrict__ counters, int poison) {
   constexpr int T = D / 8;  // threads per row, 16 B each
   const size_t gtid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const size_t rows = static_cast<size_t>(B) * N * H;
@@ -976,10 +882,14 @@ __global__ void dash_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
   }
   const size_t nthreads = static_cast<size_t>(gridDim.x) * blockDim.x;
   if (gtid == 0) {
-    *job_counter = 0;
+    counters[0] = 0;  // job counter
+    counters[1] = 0;  // error flag (dash_check_workspace reports this call only)
     ptx::g_dash_abort = 0;
   }
-  for (size_t i = gtid; i < static_cast<size_t>(n_zero_i32); i += nthreads) zero_i32[i] = 0;
+  // tickets := 0; `poison` != 0 (fault injection, dash_attn_bwd_inject_fault
+  // only) presets the first ticket to a value no add ever reaches.
+  for (size_t i = gtid; i < static_cast<size_t>(n_zero_i32); i += nthreads)
+    zero_i32[i] = (i == 0) ? poison : 0;
   for (size_t i = gtid; i < n_zero_f4; i += nthreads) zero_f32[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 

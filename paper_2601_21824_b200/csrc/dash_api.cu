@@ -10,13 +10,13 @@
 #include <cstring>
 #include <algorithm>
 #include <map>
+#include <set>
 #include <mutex>
 #include <tuple>
 #include <vector>
 
 #include "bwd.cuh"
 #include "dash.h"
-#include "fwd.cuh"
 #include "fwd_tc.cuh"
 #include "schedule.h"
 
@@ -26,7 +26,6 @@ namespace dash {
 namespace {
 
 constexpr size_t kAlign = 1024;
-constexpr int kDefaultVariant = 3;  // BwdCfg smem variant used unless DASH_VARIANT is set
 // Interleaved dQ accumulators (AMB-27): 0 = automatic (the default), else
 // fixed W in {1, 2, 4, 8}; DASH_ACC_SPLIT overrides the default at load time.
 int g_acc_split = [] {
@@ -113,34 +112,64 @@ bool aligned16(const void* p) { return p && (reinterpret_cast<uintptr_t>(p) & 15
 float eff_scale(const dash_shape* s) {
   return s->softmax_scale > 0.f ? s->softmax_scale : 1.0f / std::sqrt(static_cast<float>(s->head_dim));
 }
-// ticket granularity for the workspace: the smallest staging unit of any variant
-int ticket_rows(int d) { return d == 128 ? BwdCfg<128, 2>::STG_ROWS : BwdCfg<64, 2>::STG_ROWS; }
+// One ticket per (accumulator, b, h, Q sub-tile of BR rows).
+int ticket_rows(int d) { return d == 128 ? BwdCfg<128>::STG_ROWS : BwdCfg<64>::STG_ROWS; }
+
+// W the backward uses: the setting (automatic: per n) when deterministic, one
+// accumulator for the atomic variant.  Resolved once per call and passed to
+// both the main kernel and the convert kernel.
+int resolved_split(const dash_shape* s, int deterministic) {
+  return deterministic ? acc_split_for(s->seqlen / 128) : 1;
+}
 
 struct WsLayout {
   size_t dqacc = 0, dvec = 0, lse2 = 0, tickets = 0, counters = 0, total = 0;
   size_t dqacc_bytes = 0, n_tickets = 0;
+  int planes = 1;
 };
-// Up to kMaxSplit interleaved fp32 accumulators (AMB-27), each with its own
-// ticket set: dqacc [W][B,H,N,d], tickets [W][B*H][N / ticket_rows].
-constexpr int kMaxSplit = 8;
-WsLayout ws_layout(const dash_shape* s) {
+// W interleaved fp32 accumulators (AMB-27), each with its own ticket set:
+// dqacc [W][B,H,N,d], tickets [W][B*H][N / ticket_rows].  The accumulators
+// come first (offset 0), so a verification test can read them back.
+WsLayout ws_layout(const dash_shape* s, int W) {
   WsLayout w;
+  w.planes = W;
   const size_t BHN = static_cast<size_t>(s->batch) * s->heads * s->seqlen;
   w.dqacc_bytes = BHN * s->head_dim * 4;
   w.n_tickets = static_cast<size_t>(s->batch) * s->heads * (s->seqlen / ticket_rows(s->head_dim));
   size_t off = 0;
   w.dqacc = off;
-  off = align_up(off + kMaxSplit * w.dqacc_bytes, kAlign);
+  off = align_up(off + static_cast<size_t>(W) * w.dqacc_bytes, kAlign);
   w.dvec = off;
   off = align_up(off + BHN * 4, kAlign);
   w.lse2 = off;
   off = align_up(off + BHN * 4, kAlign);
   w.tickets = off;
-  off = align_up(off + kMaxSplit * w.n_tickets * 4, kAlign);
+  off = align_up(off + static_cast<size_t>(W) * w.n_tickets * 4, kAlign);
   w.counters = off;  // [0] job counter, [1] error flag
   off = align_up(off + 64, kAlign);
   w.total = off;
   return w;
+}
+
+// Ticket-wait watchdog (clock64 cycles): default ~35 s at 1.965 GHz.
+long long g_spin_bound = 8 * ptx::kWatchdogCycles;
+// Fault injection for the watchdog test (dash_attn_bwd_inject_fault): the
+// value the first ticket is preset to by the next backward on this thread.
+thread_local int g_poison = 0;
+
+// cudaFuncSetAttribute is per device: remember which (device, kernel) pairs
+// already have the large dynamic shared-memory limit.
+bool ensure_smem_attr(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({dev, kern})) return true;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return false;
+  done.insert({dev, kern});
+  return true;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -254,13 +283,17 @@ void prof_mark(cudaStream_t st) {
   p.ev.push_back(e);
 }
 
-template <int D, int V>
+template <int D>
 dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const void* v,
                        const void* o, const void* dout, const float* lse, void* dq, void* dk,
                        void* dv, int causal, int schedule, int deterministic, void* workspace,
-                       cudaStream_t stream) {
-  using C = BwdCfg<D, V>;
+                       size_t workspace_bytes, cudaStream_t stream) {
+  using C = BwdCfg<D>;
   const int n = s->seqlen / 128;
+  const int W = resolved_split(s, deterministic);  // once per call: K2 and K4 agree
+  const WsLayout w = ws_layout(s, W);
+  // The setting may have changed since the workspace was sized.
+  if (workspace_bytes < w.total) return DASH_ERR_WORKSPACE;
   const ScheduleTable* tab = cached_schedule(schedule, n, causal ? kCausal : kFull);
   if (!tab) return DASH_ERR_UNSUPPORTED;
   int dev = 0;
@@ -269,16 +302,11 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
   const int G = head_group_for(s);
   const int total_jobs = tab->jobs * (s->batch * s->heads / G);
   int grid = total_jobs < sms ? total_jobs : sms;
-  static const int debug_bits = [] {
-    const char* e = std::getenv("DASH_DEBUG");
-    return e ? std::atoi(e) : 0;
-  }();
 
   if (schedule == kShift && tab->coresident > grid) return DASH_ERR_UNSUPPORTED;
   const DevTable* dt = device_table(dev, tab, G);
   if (!dt) return DASH_ERR_CUDA;
 
-  const WsLayout w = ws_layout(s);
   char* ws = static_cast<char*>(workspace);
   float* dqacc = reinterpret_cast<float*>(ws + w.dqacc);
   float* dvec = reinterpret_cast<float*>(ws + w.dvec);
@@ -292,16 +320,25 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
   bool ok = make_map_2d(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, q, HD, BN, 64, C::BR) &&
             make_map_2d(&tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, k, HD, BN, 64, C::BC) &&
             make_map_2d(&tv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, v, HD, BN, 64, C::BC) &&
-            make_map_2d(&tdo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, HD, BN, 64, C::BR) &&
-            make_map_2d(&tacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dqacc, D,
-                        kMaxSplit * BN * static_cast<uint64_t>(s->heads), 32, C::STG_ROWS);
+            make_map_2d(&tdo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, HD, BN, 64, C::BR);
+  if (ok && !C::LINEAR)  // d = 64 reduces through a 2-D map of the W planes
+    ok = make_map_2d(&tacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dqacc, D,
+                     static_cast<uint64_t>(W) * BN * static_cast<uint64_t>(s->heads), 32,
+                     C::STG_ROWS);
+  else
+    tacc = tq;  // unused at d = 128 (1-D bulk reduces)
   if (!ok) {  // tensor map encoding (reported as -1 by dash_last_cuda_error)
     g_last_cuda = -1;
     return DASH_ERR_CUDA;
   }
+  auto kern = dash_bwd_kernel<D>;
+  if (!ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(C::SMEM_BYTES)))
+    return cuda_check_last();
 
+  const int poison = g_poison;
+  g_poison = 0;
   prof_mark(stream);
-  // K1: D, ticket / counter reset, dQacc zero-fill for the atomic variant.
+  // K1: D, ticket / counter / error-flag reset, dQacc zero-fill for the atomic variant.
   {
     const size_t rows = BN * s->heads;
     const size_t threads = rows * (D / 8);
@@ -309,9 +346,9 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     const unsigned gridp = static_cast<unsigned>((threads + block - 1) / block);
     dash_preprocess_kernel<D><<<gridp, block, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse, dvec,
-        lse2, s->batch, s->seqlen, s->heads, tickets, static_cast<int>(kMaxSplit * w.n_tickets),
+        lse2, s->batch, s->seqlen, s->heads, tickets, static_cast<int>(W * w.n_tickets),
         deterministic ? nullptr : reinterpret_cast<float4*>(dqacc),
-        deterministic ? 0 : w.dqacc_bytes / 16, counters);
+        deterministic ? 0 : w.dqacc_bytes / 16, counters, poison);
   }
   prof_mark(stream);
   // K2: the persistent ordered-reduction backward.
@@ -337,34 +374,28 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     a.deterministic = deterministic ? 1 : 0;
     a.trace = g_trace;
     a.trace_cap = g_trace_cap;
-    a.debug = debug_bits;
-    a.split = deterministic ? acc_split_for(n) : 1;
+    a.spin_bound = g_spin_bound;
+    a.split = W;
     a.dqacc = dqacc;
     a.n_tickets = static_cast<int>(w.n_tickets);
     a.dump = g_dump;
     static const int no_prefetch = [] {
-      const char* e = std::getenv("DASH_NO_PREFETCH");  // experiments only
+      const char* e = std::getenv("DASH_NO_PREFETCH");  // experiments only (bit-exact either way)
       return e ? std::atoi(e) : 0;
     }();
     // Early claim of the next job (bwd.cuh, producer) -- measured per schedule
-    // (profiles/r01_experiments/prefetch_claim.txt, bench r01f): it pays for
-    // the atomic variant (no waits) and for DESCENDING with W = 4 interleaved
+    // (profiles/r01_experiments/prefetch_claim.txt): it pays for the atomic
+    // variant (no waits) and for DESCENDING with W >= 4 interleaved
     // accumulators (automatic at n >= 64; its waits sit at each job's first Q
-    // tile); with W = 1 (config-5 model check) it is slower;
-    // it costs up to 2x where a claimed job, queued behind its CTA's reduction
-    // tail, stalls a chain of later jobs -- SHIFT (a head's cyclic jobs must
-    // run together), NAIVE causal (staircase) and DESCENDING with W = 2 at
-    // d = 64.  NAIVE keeps the claim-after-release of the FA3-style baseline.
+    // tile); with W = 1 (config-5 model check) it is slower; it costs up to 2x
+    // where a claimed job, queued behind its CTA's reduction tail, stalls a
+    // chain of later jobs -- SHIFT (a head's cyclic jobs must run together),
+    // NAIVE causal (staircase) and DESCENDING with W = 2 at d = 64.  NAIVE keeps
+    // the claim-after-release of the FA3-style baseline.
     a.prefetch =
         (!no_prefetch && (!deterministic || (schedule == kDescending && a.split >= 4))) ? 1 : 0;
     a.cyclic = (deterministic && schedule == kShift) ? 1 : 0;
     a.head_group = G;
-    auto kern = dash_bwd_kernel<D, V>;
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-      attr_set = true;
-    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(C::NTHREADS);
@@ -382,15 +413,15 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     }
   }
   prof_mark(stream);
-  // K4: dQ = bf16(scale * dQacc).
+  // K4: dQ = bf16(scale * (acc_0 + ... + acc_{W-1})).
   {
     const size_t total = BN * s->heads * (D / 8);
     const int block = 256;
     size_t g = (total + block - 1) / block;
     if (g > static_cast<size_t>(sms) * 16) g = static_cast<size_t>(sms) * 16;
     dash_dq_convert_kernel<D><<<static_cast<unsigned>(g), block, 0, stream>>>(
-        dqacc, static_cast<__nv_bfloat16*>(dq), s->batch, s->seqlen, s->heads, eff_scale(s),
-        deterministic ? acc_split_for(s->seqlen / 128) : 1, causal ? 1 : 0);
+        dqacc, static_cast<__nv_bfloat16*>(dq), s->batch, s->seqlen, s->heads, eff_scale(s), W,
+        causal ? 1 : 0);
   }
   prof_mark(stream);
   return cuda_check_last();
@@ -478,12 +509,9 @@ dash_status launch_fwd_tc(const dash_shape* s, const void* q, const void* k, con
   a.H = s->heads;
   a.scale_log2 = eff_scale(s) * 1.4426950408889634f;
   a.causal = causal ? 1 : 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dash_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(C::SMEM_BYTES));
-    attr = true;
-  }
+  if (!ensure_smem_attr(reinterpret_cast<const void*>(dash_fwd_tc_kernel<D>),
+                        static_cast<int>(C::SMEM_BYTES)))
+    return cuda_check_last();
   const dim3 grid(s->seqlen / 128, s->batch * s->heads);
   dash_fwd_tc_kernel<D><<<grid, 256, C::SMEM_BYTES, st>>>(tq, tk, tv, a);
   return cuda_check_last();
@@ -498,40 +526,16 @@ DASH_API dash_status dash_attn_fwd(const dash_shape* s, const void* q, const voi
       !aligned16(lse))
     return DASH_ERR_INVALID_ARG;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const float sc = eff_scale(s);
-  // tcgen05 forward (fwd_tc.cuh) unless DASH_FWD_SIMT=1 selects the fp32 SIMT
-  // kernel (fwd.cuh), kept as a second, independent GPU implementation.
-  static const int simt = [] {
-    const char* e = std::getenv("DASH_FWD_SIMT");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (!simt) return s->head_dim == 128 ? launch_fwd_tc<128>(s, q, k, v, o, lse, causal, st)
-                                       : launch_fwd_tc<64>(s, q, k, v, o, lse, causal, st);
-  const dim3 grid(s->seqlen / 64, s->batch * s->heads);
-  if (s->head_dim == 128) {
-    const size_t smem = 2 * 64 * 128 * 4;
-    cudaFuncSetAttribute(dash_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dash_fwd_kernel<128><<<grid, 256, smem, st>>>(
-        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
-        static_cast<const __nv_bfloat16*>(v), static_cast<__nv_bfloat16*>(o), lse, s->batch,
-        s->seqlen, s->heads, sc, causal ? 1 : 0);
-  } else {
-    const size_t smem = 2 * 64 * 64 * 4;
-    dash_fwd_kernel<64><<<grid, 256, smem, st>>>(
-        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
-        static_cast<const __nv_bfloat16*>(v), static_cast<__nv_bfloat16*>(o), lse, s->batch,
-        s->seqlen, s->heads, sc, causal ? 1 : 0);
-  }
-  return cuda_check_last();
+  return s->head_dim == 128 ? launch_fwd_tc<128>(s, q, k, v, o, lse, causal, st)
+                             : launch_fwd_tc<64>(s, q, k, v, o, lse, causal, st);
 }
 
 DASH_API size_t dash_attn_bwd_workspace_bytes(const dash_shape* s, int causal, int schedule,
                                               int deterministic) {
   (void)causal;
   (void)schedule;
-  (void)deterministic;
   if (!shape_ok(s)) return 0;
-  return ws_layout(s).total;
+  return ws_layout(s, resolved_split(s, deterministic)).total;
 }
 
 DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const void* k, const void* v,
@@ -544,30 +548,24 @@ DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const voi
   for (const void* p : ptrs)
     if (!aligned16(p)) return DASH_ERR_INVALID_ARG;
   if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_AUTO) return DASH_ERR_INVALID_ARG;
-  if (workspace_bytes < ws_layout(s).total) return DASH_ERR_WORKSPACE;
   if (schedule == DASH_SCHED_AUTO) schedule = auto_schedule(s, causal);
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // smem variant (BwdCfg): DASH_VARIANT overrides the default (experiments)
-  static const int variant = [] {
-    const char* e = std::getenv("DASH_VARIANT");
-    return e ? std::atoi(e) : -1;
-  }();
-  const int var = variant >= 0 ? variant : kDefaultVariant;
-#define DASH_LAUNCH(DD, VV)                                                                   \
-  launch_bwd<DD, VV>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule, deterministic, \
-                     workspace, st)
-  if (s->head_dim == 128)
-    return var == 6   ? DASH_LAUNCH(128, 6)
-           : var == 5 ? DASH_LAUNCH(128, 5)
-           : var == 4 ? DASH_LAUNCH(128, 4)
-           : var == 3 ? DASH_LAUNCH(128, 3)
-           : var == 2 ? DASH_LAUNCH(128, 2)
-           : var == 1 ? DASH_LAUNCH(128, 1)
-                      : DASH_LAUNCH(128, 0);
-  return var == 2 ? DASH_LAUNCH(64, 2)
-         : var == 1 ? DASH_LAUNCH(64, 1)
-                    : DASH_LAUNCH(64, 0);
-#undef DASH_LAUNCH
+  return s->head_dim == 128
+             ? launch_bwd<128>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule,
+                               deterministic, workspace, workspace_bytes, st)
+             : launch_bwd<64>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule,
+                              deterministic, workspace, workspace_bytes, st);
+}
+
+DASH_API dash_status dash_attn_bwd_set_watchdog(long long cycles) {
+  if (cycles < 0) return DASH_ERR_INVALID_ARG;
+  g_spin_bound = cycles == 0 ? 8 * ptx::kWatchdogCycles : cycles;
+  return DASH_OK;
+}
+
+DASH_API dash_status dash_attn_bwd_inject_fault(int poison) {
+  g_poison = poison;
+  return DASH_OK;
 }
 
 DASH_API dash_status dash_attn_bwd_trace(const dash_shape* s, const void* q, const void* k,
@@ -645,7 +643,7 @@ struct HostPlan {
   size_t in_bytes, lse_bytes;  // per chunk (largest)
   size_t q, k, v, o, dout, lse, dq, dk, dv, inner, slot, total;
 };
-HostPlan host_plan(const dash_shape* s) {
+HostPlan host_plan(const dash_shape* s, int deterministic) {
   HostPlan h;
   const int kc = host_chunks();
   if (s->batch >= kc) {
@@ -672,7 +670,7 @@ HostPlan host_plan(const dash_shape* s) {
   h.lse = off;
   off = align_up(off + h.lse_bytes, kAlign);
   h.inner = off;
-  h.slot = align_up(off + ws_layout(&cs).total, kAlign);
+  h.slot = align_up(off + ws_layout(&cs, resolved_split(&cs, deterministic)).total, kAlign);
   h.total = kHostSlots * h.slot;
   return h;
 }
@@ -725,9 +723,8 @@ DASH_API size_t dash_attn_bwd_host_workspace_bytes(const dash_shape* s, int caus
                                                    int deterministic) {
   (void)causal;
   (void)schedule;
-  (void)deterministic;
   if (!shape_ok(s)) return 0;
-  return host_plan(s).total;
+  return host_plan(s, deterministic).total;
 }
 
 DASH_API dash_status dash_attn_bwd_host(const dash_shape* s, const void* q, const void* k,
@@ -741,7 +738,7 @@ DASH_API dash_status dash_attn_bwd_host(const dash_shape* s, const void* q, cons
   for (const void* p : hptrs)
     if (!p) return DASH_ERR_INVALID_ARG;
   if (!aligned16(workspace)) return DASH_ERR_INVALID_ARG;
-  const HostPlan h = host_plan(s);
+  const HostPlan h = host_plan(s, deterministic);
   if (workspace_bytes < h.total) return DASH_ERR_WORKSPACE;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return DASH_ERR_CUDA;
@@ -805,21 +802,15 @@ DASH_API dash_status dash_check_workspace(const dash_shape* s, int causal, int s
                                           int deterministic, const void* workspace, void* stream) {
   (void)causal;
   (void)schedule;
-  (void)deterministic;
   if (!shape_ok(s) || !workspace) return DASH_ERR_INVALID_ARG;
-  const WsLayout w = ws_layout(s);
+  const WsLayout w = ws_layout(s, resolved_split(s, deterministic));
   int flag = 0;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   int* dflag = reinterpret_cast<int*>(static_cast<char*>(const_cast<void*>(workspace)) + w.counters) + 1;
   if (cudaMemcpyAsync(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return DASH_ERR_CUDA;
   if (cudaStreamSynchronize(st) != cudaSuccess) return DASH_ERR_CUDA;
-  if (flag) {
-    cudaMemsetAsync(dflag, 0, sizeof(int), st);
-    cudaStreamSynchronize(st);
-    return DASH_ERR_DEADLOCK;
-  }
-  return DASH_OK;
+  return flag ? DASH_ERR_DEADLOCK : DASH_OK;
 }
 
 DASH_API dash_status dash_schedule_critical_path(int schedule, int n_q, int n_kv, int mask,

@@ -203,6 +203,53 @@ __global__ void __launch_bounds__(128, 1) probe_mma_rate_kernel(int reps, long l
   if (warp == 0) ptx::tmem_dealloc<512>(tb);
 }
 
+// TMEM <-> register throughput: NW warps (warp w reads lane quarter w % 4),
+// each doing `reps` rounds of `inflight` tcgen05.ld.32x32b.x32 (4 KB per warp
+// each) followed by one wait::ld (MODE 0), or tcgen05.st.32x32b.x16 + wait::st
+// (MODE 1).  out[blockIdx.x] = cycles per round of the slowest warp, so an
+// SM-wide figure is NW * inflight * 4 KB (ld) / cycles.
+template <int MODE, int INFLIGHT>
+__global__ void __launch_bounds__(512, 1) probe_tmem_rate_kernel(int reps, long long* out) {
+  __shared__ uint32_t tmem_base;
+  __shared__ long long worst;
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
+  if (warp == 0) ptx::tmem_alloc<512>(&tmem_base);
+  if (threadIdx.x == 0) worst = 0;
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tb = tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+  float acc = 0.f;
+  const long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    if (MODE == 0) {
+      float v[INFLIGHT][32];
+#pragma unroll
+      for (int i = 0; i < INFLIGHT; ++i) ptx::tmem_ld32(tb + ((warp >> 2) * 128 + i * 32) % 512, v[i]);
+      ptx::tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < INFLIGHT; ++i) acc += v[i][i & 31];
+    } else {
+      uint32_t v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = static_cast<uint32_t>(r + i);
+#pragma unroll
+      for (int i = 0; i < INFLIGHT; ++i) ptx::tmem_st16(tb + ((warp >> 2) * 128 + i * 16) % 512, v);
+      ptx::tmem_wait_st();
+    }
+  }
+  const long long t1 = clock64();
+  if (acc == 12345.f) out[0] = -1;  // keep the loads alive
+  atomicMax(reinterpret_cast<unsigned long long*>(&worst), static_cast<unsigned long long>(t1 - t0));
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) out[blockIdx.x] = worst / reps;
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem_base);
+  }
+}
+
 // Throughput of adding a 32 KB fp32 tile (64 rows x 128) per iteration into
 // a private global region: mode 0 = red.global.add.v4.f32 from 128 threads,
 // mode 1 = same + membar.gl per iteration (ordered hand-off cost).
@@ -347,6 +394,70 @@ extern "C" __attribute__((visibility("default"))) int dash_probe_mma_rate(int n,
   RATE_CASE(128)
   RATE_CASE(256)
 #undef RATE_CASE
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return static_cast<int>(e);
+}
+
+// MUFU ex2 vs FMA-pipe polynomial exp2 throughput: each thread runs `reps`
+// rounds over 8 independent values.  MODE 0: ex2.approx.ftz.f32; MODE 1: a
+// degree-3 polynomial 2^x (floor/fraction split, FFMA Horner, exponent add)
+// as in FlashAttention-4's software exp2.  out = cycles per round per CTA.
+template <int MODE>
+__global__ void __launch_bounds__(1024, 1) probe_exp_rate_kernel(int reps, float* sink, long long* out) {
+  float x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = -0.001f * (threadIdx.x + i);
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float y;
+      if (MODE == 0) {
+        asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x[i]));
+      } else {
+        const float xf = fmaxf(x[i], -127.f);
+        const float fl = floorf(xf);
+        const float f = xf - fl;
+        float p = fmaf(f, 0.0555041086648216f, 0.2402264923172050f);
+        p = fmaf(p, f, 0.6931471805599453f);
+        p = fmaf(p, f, 1.0f);
+        y = __int_as_float(__float_as_int(p) + (static_cast<int>(fl) << 23));
+      }
+      x[i] = y - 1.0f;
+    }
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 12345.f) sink[threadIdx.x] = s;
+  if (threadIdx.x == 0) out[blockIdx.x] = (t1 - t0) / reps;
+}
+
+extern "C" __attribute__((visibility("default"))) int dash_probe_exp_rate(int mode, int nthreads,
+                                                                         int reps, int grid,
+                                                                         float* sink,
+                                                                         long long* out) {
+  if (mode == 0) probe_exp_rate_kernel<0><<<grid, nthreads>>>(reps, sink, out);
+  else probe_exp_rate_kernel<1><<<grid, nthreads>>>(reps, sink, out);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return static_cast<int>(e);
+}
+
+extern "C" __attribute__((visibility("default"))) int dash_probe_tmem_rate(int mode, int inflight,
+                                                                          int nwarps, int reps,
+                                                                          int grid,
+                                                                          long long* out) {
+  auto launch = [&](auto kern) { kern<<<grid, nwarps * 32>>>(reps, out); };
+  if (mode == 0 && inflight == 1) launch(probe_tmem_rate_kernel<0, 1>);
+  if (mode == 0 && inflight == 2) launch(probe_tmem_rate_kernel<0, 2>);
+  if (mode == 0 && inflight == 4) launch(probe_tmem_rate_kernel<0, 4>);
+  if (mode == 1 && inflight == 1) launch(probe_tmem_rate_kernel<1, 1>);
+  if (mode == 1 && inflight == 4) launch(probe_tmem_rate_kernel<1, 4>);
   cudaError_t e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = cudaGetLastError();
   return static_cast<int>(e);

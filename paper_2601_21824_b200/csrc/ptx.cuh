@@ -111,6 +111,14 @@ __device__ __forceinline__ void mbar_wait_u(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ bool aborted() {
   return *reinterpret_cast<volatile int*>(&g_dash_abort) != 0;
 }
+// Exit-path wait that ignores the abort flag (so asynchronous TMA writes /
+// MMAs a CTA issued are complete before it retires, even after an abort),
+// bounded by ~2^26 cycles so it can never hang.
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
+  const long long t0 = clock64();
+  while (!mbar_try_wait(bar, parity))
+    if (clock64() - t0 > (1ll << 26)) return;
+}
 
 // ---- proxy fences -----------------------------------------------------------
 __device__ __forceinline__ void fence_async_smem() {

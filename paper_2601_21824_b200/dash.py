@@ -89,6 +89,10 @@ def _load():
     lib.dash_profile_end.argtypes = [dp, dp, dp, ctypes.POINTER(ctypes.c_int)]
     lib.dash_attn_bwd_launches.restype = i
     lib.dash_attn_bwd_launches.argtypes = [i, i, i]
+    lib.dash_attn_bwd_set_watchdog.restype = st
+    lib.dash_attn_bwd_set_watchdog.argtypes = [ctypes.c_longlong]
+    lib.dash_attn_bwd_inject_fault.restype = st
+    lib.dash_attn_bwd_inject_fault.argtypes = [i]
     return lib
 
 
@@ -303,3 +307,14 @@ def profile_end():
 
 def bwd_launches(causal, schedule, deterministic) -> int:
     return int(_lib.dash_attn_bwd_launches(int(causal), _sched(schedule), int(deterministic)))
+
+
+def set_watchdog(cycles: int):
+    """dash_attn_bwd_set_watchdog: bound of one ticket wait in clock64 cycles (0 = default)."""
+    _check(_lib.dash_attn_bwd_set_watchdog(int(cycles)), "dash_attn_bwd_set_watchdog")
+
+
+def inject_fault(poison: int):
+    """dash_attn_bwd_inject_fault (verification only): the next backward on this
+    thread presets its first ticket to `poison`, a value no ordered add reaches."""
+    _check(_lib.dash_attn_bwd_inject_fault(int(poison)), "dash_attn_bwd_inject_fault")

@@ -58,3 +58,52 @@ def per_head_digests(t: torch.Tensor) -> list[str]:
     """SHA-256 per head of a [B, N, H, d] tensor, ordered by (b, h)."""
     B, _, H, _ = t.shape
     return [digest(t[b, :, h]) for b in range(B) for h in range(H)]
+
+
+# --- flattened (b, h) units: the strong-scaling split of SURVEY.md §8(e) -----
+
+def unit_range(U: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced split of U = B*H flattened units u = b*H + h."""
+    return head_range(U, world, rank)
+
+
+def unit_slices(B: int, H: int, world: int, rank: int) -> list[tuple[int, int, int]]:
+    """The rank's units as (b, h0, h1) runs -- one run per batch it touches."""
+    u0, u1 = unit_range(B * H, world, rank)
+    runs = []
+    u = u0
+    while u < u1:
+        b, h0 = divmod(u, H)
+        h1 = min(H, h0 + (u1 - u))
+        runs.append((b, h0, h1))
+        u += h1 - h0
+    return runs
+
+
+def shard_units(t: torch.Tensor, world: int, rank: int, layout: str = "bnhd") -> torch.Tensor:
+    """Rank's units of a [B, N, H, d] ("bnhd") or [B, H, N] ("bhn") tensor as
+    one contiguous [B_r, N, H_r, d] / [B_r, H_r, N] tensor.  The units must
+    form whole batches or one head range of a single batch (always true when
+    world divides B*H and both are powers of two, as in every BASELINE
+    config); otherwise ValueError."""
+    if layout == "bnhd":
+        B, _, H, _ = t.shape
+    elif layout == "bhn":
+        B, H, _ = t.shape
+    else:
+        raise ValueError(layout)
+    runs = unit_slices(B, H, world, rank)
+    if not runs:
+        raise ValueError("empty shard")
+    if all(h0 == 0 and h1 == H for _, h0, h1 in runs):
+        b0, b1 = runs[0][0], runs[-1][0] + 1
+        return t[b0:b1].contiguous()
+    if len(runs) == 1:
+        b, h0, h1 = runs[0]
+        return (t[b:b + 1, :, h0:h1] if layout == "bnhd" else t[b:b + 1, h0:h1]).contiguous()
+    raise ValueError("units do not form a rectangular [B_r, H_r] block")
+
+
+def per_unit_digests(t: torch.Tensor) -> list[str]:
+    """SHA-256 per (b, h) unit of a [B, N, H, d] tensor, in flattened order."""
+    return per_head_digests(t)

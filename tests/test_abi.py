@@ -166,3 +166,31 @@ def test_auto_schedule_policy_and_acc_split(dash):
         dash.set_acc_split(old)
     with pytest.raises(dash.DashError):  # AUTO is not a schedule of the DAG model
         dash.schedule_critical_path(dash.AUTO, 4, 4, dash.CAUSAL)
+
+
+def test_critical_path_every_n_4_to_128(dash):
+    """BASELINE configs[4] (AMB-20): for every n_q = n_kv in 4..128, both masks
+    and all three schedules, the product's DAG model equals the oracle's
+    brute-force simulator bit for bit -- at the SURVEY default (m = 2, n_sm =
+    n, c = r = 1) and at a c > r point with four heads -- and, where the paper
+    states a closed form (AMB-8/9/10), both equal it.
+    SHIFT causal with odd n runs the AMB-29 schedule (no closed form)."""
+    for n in range(4, 129):
+        for mask in (dag.FULL, dag.CAUSAL):
+            for schedule in (dag.NAIVE, dag.DESCENDING, dag.SHIFT):
+                for m, c, r in ((2, 1, 1), (4, 3, 1)):
+                    want = dag.simulate(schedule, n, mask, m, n, c, r)
+                    got = dash.schedule_critical_path(schedule, n, n, mask, m, n, c, r)
+                    assert got == want, (schedule, mask, n, m, c, r)
+                    if schedule == dag.NAIVE or (schedule == dag.DESCENDING and mask == dag.FULL):
+                        form = m * n * (c + r) + (n - 1) * r
+                    elif schedule == dag.DESCENDING:                   # c >= r here (AMB-9)
+                        form = m * (n + 1) * (c + r) // 2 + (n - 1) * r
+                    elif mask == dag.FULL:
+                        form = m * n * (c + r)
+                    elif n % 2 == 0:
+                        form = ((m + 1) // 2) * (n + 1) * (c + r)
+                    else:
+                        form = None
+                    if form is not None:
+                        assert got == form, (schedule, mask, n, m, c, r)

@@ -340,3 +340,34 @@ def test_long_context_config4_sampled_rows(dash):
         for x, r in ((dk[b, rows, h], rk[0]), (dv[b, rows, h], rv[0])):
             x = x.double().cpu().numpy()
             assert np.max(np.abs(x - r)) / np.max(np.abs(r)) <= GRAD_TOL
+
+
+@pytest.mark.parametrize("schedule,causal,N", [
+    ("descending", True, 8192),   # W = 4 and early claim of the next job (prefetch on)
+    ("shift", False, 1024),       # cyclic waits inside a head (claim after release)
+])
+def test_watchdog_reports_deadlock_and_recovers(dash, schedule, causal, N):
+    """A ticket that never reaches its rank (fault injection: the first ticket
+    preset to 1 << 30) must trip the bounded ticket wait, make every warp role
+    leave (the kernel returns), and be reported as DASH_ERR_DEADLOCK by
+    dash_check_workspace; the next call on the same workspace (K1 resets the
+    error flag) is correct again (Alg. 1 lines 33-35)."""
+    B, H, d = 1, 4, 128
+    _, g = _inputs(B, N, H, d, seed=8)
+    o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], causal)
+    ws = dash.alloc_workspace(g["q"].shape, causal, schedule, True)
+    good = [t.clone() for t in dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal,
+                                             schedule, True, workspace=ws)]
+    assert dash.check_workspace(g["q"].shape, causal, schedule, True, ws) == dash.OK
+    dash.set_watchdog(1 << 24)  # ~8.5 ms at 1.965 GHz
+    try:
+        dash.inject_fault(1 << 30)
+        dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal, schedule, True, workspace=ws)
+        assert dash.check_workspace(g["q"].shape, causal, schedule, True, ws) == dash.ERR_DEADLOCK
+    finally:
+        dash.set_watchdog(0)
+    again = dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal, schedule, True,
+                          workspace=ws)
+    assert dash.check_workspace(g["q"].shape, causal, schedule, True, ws) == dash.OK
+    for a, b in zip(again, good):
+        assert torch.equal(a, b)

@@ -54,7 +54,30 @@ def acc_split(request, dash):
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("schedule", ["naive", "descending", "shift"])
 def test_dq_equals_host_resum_in_paper_order(dash, acc_split, N, d, causal, schedule):
-    B, H = 1, 2
+    _replay(dash, acc_split, 1, N, 2, d, causal, schedule)
+
+
+@pytest.mark.parametrize("W", [4, 8])
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("schedule", ["naive", "descending", "shift"])
+def test_replay_every_plane_live(dash, W, d, causal, schedule):
+    """n = 17 KV tiles (N = 2176): with W = 8 every accumulator plane of every
+    Q tile with >= 2W + 1 contributors receives >= 2 ordered adds (the
+    ticket-order path, not just the rank-0 store); the busiest tiles
+    (17 contributors) give plane 0 three adds and planes 1-7 two."""
+    old = dash.acc_split()
+    dash.set_acc_split(W)
+    try:
+        per_plane = _replay(dash, W, 1, 2176, 1, d, causal, schedule)
+    finally:
+        dash.set_acc_split(old)
+    assert all(c >= 2 for c in per_plane[:W]), per_plane
+
+
+def _replay(dash, W, B, N, H, d, causal, schedule):
+    """Re-sum the dumped partials in the paper's order, compare bits; returns,
+    per accumulator plane, the largest number of adds it received in one tile."""
     T = 128                                                # schedule tile rows (AMB-11)
     n = N // T
     mask = dag.CAUSAL if causal else dag.FULL
@@ -65,8 +88,7 @@ def test_dq_equals_host_resum_in_paper_order(dash, acc_split, N, d, causal, sche
                                                schedule, True)
     torch.cuda.synchronize()
     parts = parts.cpu().numpy()                                        # [B*H, N/128, N, d] fp32
-    W = acc_split                                                      # AMB-27
-    assert dash.acc_split(N) == W
+    assert dash.acc_split(N) == W                                      # AMB-27
     acc_gpu = ws[: W * B * H * N * d * 4].view(torch.float32).cpu().numpy().reshape(W, B * H, N, d)
     dq_bits = dq.view(torch.int16).cpu().numpy().view(np.uint16)     # [B, N, H, d]
     scale = np.float32(1.0) / np.sqrt(np.float32(d))
@@ -77,6 +99,7 @@ def test_dq_equals_host_resum_in_paper_order(dash, acc_split, N, d, causal, sche
         return parts[bh, i, j * T:(j + 1) * T]
 
     checked_acc = 0
+    per_plane = [0] * W
     for bh in range(B * H):
         b, h = divmod(bh, H)
         for j in range(n):
@@ -87,6 +110,7 @@ def test_dq_equals_host_resum_in_paper_order(dash, acc_split, N, d, causal, sche
             for w in range(min(W, len(order))):
                 # accumulator w: ranks w, w + W, ... in order; its first one stores
                 mine = [i for rk, i in order if rk % W == w]
+                per_plane[w] = max(per_plane[w], len(mine))
                 acc = contribution(bh, mine[0], j).copy()
                 for i in mine[1:]:
                     acc = (acc + contribution(bh, i, j)).astype(np.float32)
@@ -102,6 +126,7 @@ def test_dq_equals_host_resum_in_paper_order(dash, acc_split, N, d, causal, sche
             bad = np.count_nonzero(got != want)
             assert bad == 0, f"dq bh={bh} tile={j}: {bad} of {want.size} bf16 values differ"
     assert checked_acc > 0
+    return per_plane
 
 
 def test_partials_cover_exactly_the_visited_tiles(dash):

@@ -1,8 +1,7 @@
 """Runtime choices never change bits (DESIGN.md AMB-22, AMB-27, AMB-28).
 
-The library takes several decisions that are not part of the method: the
-staging variant of the ordered reduction (DASH_VARIANT), early claiming of
-the next job (on for DESCENDING at n >= 64 and the atomic variant; off with
+The library takes several decisions that are not part of the method: early
+claiming of the next job (on for DESCENDING at n >= 64 and the atomic variant; off with
 DASH_NO_PREFETCH=1) and head grouping (DASH_HEAD_GROUP=G: one job covers G
 heads).  None of them may change any head's Q order or reduction ranks, so
 the deterministic dq/dk/dv must be bit-identical under every setting.  The
@@ -51,7 +50,7 @@ print(json.dumps(out))
 
 def _digests(env_extra):
     env = dict(os.environ)
-    for k in ("DASH_VARIANT", "DASH_NO_PREFETCH", "DASH_HEAD_GROUP"):
+    for k in ("DASH_NO_PREFETCH", "DASH_HEAD_GROUP"):
         env.pop(k, None)
     env.update(env_extra)
     r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, json.dumps(CASES)], env=env,
@@ -73,9 +72,6 @@ def reference_digests():
     {"DASH_NO_PREFETCH": "1"},
     {"DASH_HEAD_GROUP": "2"},
     {"DASH_HEAD_GROUP": "4"},
-    {"DASH_VARIANT": "0"},
-    {"DASH_VARIANT": "5"},
-    {"DASH_VARIANT": "6"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_runtime_choice_keeps_bits(reference_digests, env):
     got = _digests(env)
