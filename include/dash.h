@@ -201,7 +201,7 @@ dash_status dash_profile_end(double* ms_preprocess, double* ms_main, double* ms_
 /* Measurement variant of dash_attn_bwd (same arguments and results) that
  * also records, per CTA of the main kernel and per Q sub-tile x it processes
  * (x < trace_cap), clock64() stamps of the pipeline stages into `trace`
- * (device memory, uint64 [grid][trace_cap][16], grid = min(jobs, SMs),
+ * (device memory, uint64 [grid][trace_cap][32], grid = min(jobs, SMs),
  * zero-filled by the caller).  Slots: 0 S/dP MMAs issued, 1 P^T/dS^T seen
  * by the MMA issuer, 2 dQ MMA issued, 3 softmax start, 4 softmax done,
  * 5 dQ drain start, 6 dQ staged, 7 ticket acquired, 8 reduce issued,
@@ -240,7 +240,8 @@ dash_status dash_attn_bwd_set_acc_split(int w);
 /* Verification variant of dash_attn_bwd (same arguments and results) that
  * also writes every dQ partial dQ_local = dS K_i (Alg.1 line 28; fp32,
  * unscaled) as it is handed to the ordered reduction: partials is device
- * memory, fp32 [B*H][n][N][d] with n = N/128 KV tiles, element
+ * memory, fp32 [B*H][n][N][d] with n = N / T KV tiles of T rows
+ * (T = dash_attn_bwd_tile(shape, causal, schedule)), element
  * [bh][i][r][c] = the partial of KV tile i for query row r (rows of Q tiles
  * that KV tile i does not visit are left untouched; zero-fill first).  With
  * the schedule's ranks this lets
@@ -248,7 +249,7 @@ dash_status dash_attn_bwd_set_acc_split(int w);
  * bit for bit (SURVEY.md §8(c) c4 "T5
  * replay").  partial_bytes must be >= dash_attn_bwd_dump_bytes(shape) (else
  * DASH_ERR_WORKSPACE); null/misaligned partials: DASH_ERR_INVALID_ARG. */
-size_t dash_attn_bwd_dump_bytes(const dash_shape* shape);
+size_t dash_attn_bwd_dump_bytes(const dash_shape* shape, int causal, int schedule);
 dash_status dash_attn_bwd_dump(const dash_shape* shape, const void* q, const void* k,
                                const void* v, const void* o, const void* dout, const float* lse,
                                void* dq, void* dk, void* dv, int causal, int schedule,
@@ -266,6 +267,20 @@ dash_status dash_attn_bwd_set_watchdog(long long cycles);
  * rank no ordered add ever reaches -- so a wait can only end through the
  * watchdog.  Always DASH_OK. */
 dash_status dash_attn_bwd_inject_fault(int poison);
+
+/* Schedule tile size T (B_r = B_c, AMB-11 / AMB-31) a dash_attn_bwd with
+ * these arguments runs with: 256 -- the CTA-pair kernel (a cluster of two
+ * CTAs per 256-row KV tile, cta_group::2 MMAs, one dQ partial per 256 KV
+ * rows) -- at d = 128 when N is a multiple of 256 (and, for SHIFT, the
+ * head's jobs fit the device's CTA pairs), else 128 (the single-CTA kernel).
+ * The schedules, ranks and the DAG model are those of the paper with n =
+ * N / T tiles.  0 for an invalid shape or schedule. */
+int dash_attn_bwd_tile(const dash_shape* shape, int causal, int schedule);
+
+/* 0 = automatic (the rule above), 128 = always the single-CTA kernel.
+ * Host-global; DASH_ERR_INVALID_ARG for other values.  DASH_TILE in the
+ * environment sets the initial value. */
+dash_status dash_attn_bwd_set_tile(int tile);
 
 /* Number of device kernel launches one dash_attn_bwd makes (for accounting):
  * 3 (preprocess, main, dQ convert). */

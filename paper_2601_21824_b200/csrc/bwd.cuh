@@ -54,7 +54,7 @@ struct BwdArgs {
   float scale_log2;
   int causal;
   int deterministic;
-  unsigned long long* trace;  // optional clock64 trace [grid][trace_cap][16] (measurement only)
+  unsigned long long* trace;  // optional clock64 trace [grid][trace_cap][32] (measurement only)
   int trace_cap;
   long long spin_bound;  // ticket-wait watchdog, clock64 cycles (dash_attn_bwd_set_watchdog)
   float* dump;  // verification only: every dQ partial, [B*H][N/128][N][d] fp32
@@ -85,7 +85,7 @@ struct BwdArgs {
 #define DASH_TRACE_MARK(slot, xx)                                                         \
   do {                                                                                    \
     if (args.trace != nullptr && static_cast<int>(xx) < args.trace_cap)                   \
-      args.trace[(static_cast<size_t>(blockIdx.x) * args.trace_cap + (xx)) * 16 + (slot)] = \
+      args.trace[(static_cast<size_t>(blockIdx.x) * args.trace_cap + (xx)) * 32 + (slot)] = \
           clock64();                                                                      \
   } while (0)
 
@@ -895,11 +895,13 @@ __global__ void dash_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
 
 // K4: dQ = bf16(scale * dQacc), [B,H,N,d] fp32 -> [B,N,H,d] bf16.  With W
 // interleaved accumulators (AMB-27) the sum is ((acc_0 + acc_1) + acc_2) + ...
-// (fp32, in index order) over the min(W, cnt) accumulators a 128-row Q tile
-// with cnt contributions has written (causal: tile j has j + 1).
+// (fp32, in index order) over the min(W, cnt) accumulators a Q tile (of
+// `tile` = 128 or 256 rows) with cnt contributions has written (causal: tile j
+// has j + 1).
 template <int D>
 __global__ void dash_dq_convert_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq,
-                                       int B, int N, int H, float scale, int split, int causal) {
+                                       int B, int N, int H, float scale, int split, int causal,
+                                       int tile) {
   constexpr int T = D / 8;
   const size_t total = static_cast<size_t>(B) * H * N * T;
   const size_t plane = static_cast<size_t>(B) * H * N * D;
@@ -913,7 +915,7 @@ __global__ void dash_dq_convert_kernel(const float* __restrict__ acc, __nv_bfloa
     const int b = static_cast<int>(bh / H);
     float4 x0 = *reinterpret_cast<const float4*>(acc + r * D + part * 8);
     float4 x1 = *reinterpret_cast<const float4*>(acc + r * D + part * 8 + 4);
-    const int cnt = causal ? n / 128 + 1 : N / 128;
+    const int cnt = causal ? n / tile + 1 : N / tile;  // contributions to this row's Q tile
     const int planes = split < cnt ? split : cnt;  // accumulator w holds ranks w, w + W, ...
     for (int w = 1; w < planes; ++w) {
       const float4 y0 = *reinterpret_cast<const float4*>(acc + w * plane + r * D + part * 8);

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "bwd.cuh"
+#include "bwd2.cuh"
 #include "dash.h"
 #include "fwd_tc.cuh"
 #include "schedule.h"
@@ -112,8 +113,40 @@ bool aligned16(const void* p) { return p && (reinterpret_cast<uintptr_t>(p) & 15
 float eff_scale(const dash_shape* s) {
   return s->softmax_scale > 0.f ? s->softmax_scale : 1.0f / std::sqrt(static_cast<float>(s->head_dim));
 }
-// One ticket per (accumulator, b, h, Q sub-tile of BR rows).
-int ticket_rows(int d) { return d == 128 ? BwdCfg<128>::STG_ROWS : BwdCfg<64>::STG_ROWS; }
+// Schedule tile size (AMB-11 / AMB-31): 256 (the CTA-pair kernel, bwd2.cuh)
+// at d = 128 when N is a multiple of 256, else 128 (the single-CTA kernel);
+// dash_attn_bwd_set_tile(128) forces the single-CTA kernel.
+int g_tile = [] {
+  const char* e = std::getenv("DASH_TILE");
+  const int v = e ? std::atoi(e) : 0;
+  return (v == 128 || v == 256) ? v : 0;
+}();
+int auto_schedule(const dash_shape* s, int causal);
+int pair_cluster_bound() {  // CTA pairs co-resident on the current device
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 74;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 2)
+    return 74;
+  return n / 2;
+}
+// `schedule` already resolved (not AUTO).  SHIFT needs a head's jobs
+// co-resident (AMB-12): with 256-row tiles that is min(n', 128) CTA pairs for
+// the full mask, ceil(n'/2) for causal -- beyond the device's pairs the
+// single-CTA kernel (128-row tiles, up to 148 co-resident CTAs) runs instead.
+int tile_for(const dash_shape* s, int causal, int schedule) {
+  const bool pair_ok = s->head_dim == 128 && s->seqlen % PairCfg::TILE == 0;
+  if (g_tile == 128 || !pair_ok) return 128;
+  if (schedule == kShift) {
+    const ScheduleTable* t = cached_schedule(kShift, s->seqlen / PairCfg::TILE, causal ? kCausal : kFull);
+    if (!t || t->coresident > pair_cluster_bound()) return 128;
+  }
+  return 256;
+}
+
+// One ticket per (accumulator, b, h, Q sub-tile of 64 / 128 rows) -- and per d
+// half for the pair kernel; sized for the largest use at this head dim.
+size_t tickets_per_head(int d, int N) { return d == 128 ? 2 * (N / 64) : N / 128; }
 
 // W the backward uses: the setting (automatic: per n) when deterministic, one
 // accumulator for the atomic variant.  Resolved once per call and passed to
@@ -135,7 +168,7 @@ WsLayout ws_layout(const dash_shape* s, int W) {
   w.planes = W;
   const size_t BHN = static_cast<size_t>(s->batch) * s->heads * s->seqlen;
   w.dqacc_bytes = BHN * s->head_dim * 4;
-  w.n_tickets = static_cast<size_t>(s->batch) * s->heads * (s->seqlen / ticket_rows(s->head_dim));
+  w.n_tickets = static_cast<size_t>(s->batch) * s->heads * tickets_per_head(s->head_dim, s->seqlen);
   size_t off = 0;
   w.dqacc = off;
   off = align_up(off + static_cast<size_t>(W) * w.dqacc_bytes, kAlign);
@@ -421,7 +454,153 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     if (g > static_cast<size_t>(sms) * 16) g = static_cast<size_t>(sms) * 16;
     dash_dq_convert_kernel<D><<<static_cast<unsigned>(g), block, 0, stream>>>(
         dqacc, static_cast<__nv_bfloat16*>(dq), s->batch, s->seqlen, s->heads, eff_scale(s), W,
-        causal ? 1 : 0);
+        causal ? 1 : 0, 128);
+  }
+  prof_mark(stream);
+  return cuda_check_last();
+}
+
+template <int NQS, int NQK, int NDS>
+int max_pair_clusters(int dev) {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * device_sms(dev));
+  cfg.blockDim = dim3(PairCfg::NTHREADS);
+  cfg.dynamicSmemBytes = PairCfgT<NQS, NQK, NDS>::SMEM_BYTES;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, dash_bwd_pair_kernel<NQS, NQK, NDS>, &cfg) != cudaSuccess ||
+      n < 1)
+    n = device_sms(dev) / 2;
+  (void)cudaGetLastError();
+  cache[dev] = n;
+  return n;
+}
+
+// The CTA-pair backward (bwd2.cuh), d = 128, 256-row schedule tiles.
+template <int NQS, int NQK, int NDS>
+dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, const void* v,
+                            const void* o, const void* dout, const float* lse, void* dq, void* dk,
+                            void* dv, int causal, int schedule, int deterministic, void* workspace,
+                            size_t workspace_bytes, cudaStream_t stream) {
+  using C = PairCfgT<NQS, NQK, NDS>;
+  constexpr int D = 128;
+  const int n = s->seqlen / C::TILE;
+  const int W = resolved_split(s, deterministic);
+  const WsLayout w = ws_layout(s, W);
+  if (workspace_bytes < w.total) return DASH_ERR_WORKSPACE;
+  const ScheduleTable* tab = cached_schedule(schedule, n, causal ? kCausal : kFull);
+  if (!tab) return DASH_ERR_UNSUPPORTED;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return DASH_ERR_CUDA;
+  auto kern = dash_bwd_pair_kernel<NQS, NQK, NDS>;
+  if (!ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(C::SMEM_BYTES)))
+    return cuda_check_last();
+  const int sms = device_sms(dev);
+  const int max_cl = max_pair_clusters<NQS, NQK, NDS>(dev);
+  const int total_jobs = tab->jobs * (s->batch * s->heads);
+  const int clusters = total_jobs < max_cl ? total_jobs : max_cl;
+  if (schedule == kShift && tab->coresident > clusters) return DASH_ERR_UNSUPPORTED;
+  const DevTable* dt = device_table(dev, tab, 1);
+  if (!dt) return DASH_ERR_CUDA;
+
+  char* ws = static_cast<char*>(workspace);
+  float* dqacc = reinterpret_cast<float*>(ws + w.dqacc);
+  float* dvec = reinterpret_cast<float*>(ws + w.dvec);
+  float* lse2 = reinterpret_cast<float*>(ws + w.lse2);
+  int* tickets = reinterpret_cast<int*>(ws + w.tickets);
+  int* counters = reinterpret_cast<int*>(ws + w.counters);
+
+  const uint64_t HD = static_cast<uint64_t>(s->heads) * D;
+  const uint64_t BN = static_cast<uint64_t>(s->batch) * s->seqlen;
+  CUtensorMap tq32, tq64, tk, tv, tdo32, tdo64, tacc;
+  const bool ok =
+      make_map_2d(&tq32, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, q, HD, BN, 64, 32) &&
+      make_map_2d(&tq64, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, q, HD, BN, 64, 64) &&
+      make_map_2d(&tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, k, HD, BN, 64, C::BC) &&
+      make_map_2d(&tv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, v, HD, BN, 64, C::BC) &&
+      make_map_2d(&tdo32, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, HD, BN, 64, 32) &&
+      make_map_2d(&tdo64, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, HD, BN, 64, 64) &&
+      make_map_2d(&tacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dqacc, D,
+                  static_cast<uint64_t>(W) * BN * static_cast<uint64_t>(s->heads), 32, C::BR);
+  if (!ok) {
+    g_last_cuda = -1;
+    return DASH_ERR_CUDA;
+  }
+  const int poison = g_poison;
+  g_poison = 0;
+  prof_mark(stream);
+  {
+    const size_t rows = BN * s->heads;
+    const size_t threads = rows * (D / 8);
+    const int block = 256;
+    const unsigned gridp = static_cast<unsigned>((threads + block - 1) / block);
+    dash_preprocess_kernel<D><<<gridp, block, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse, dvec,
+        lse2, s->batch, s->seqlen, s->heads, tickets, static_cast<int>(W * w.n_tickets),
+        deterministic ? nullptr : reinterpret_cast<float4*>(dqacc),
+        deterministic ? 0 : w.dqacc_bytes / 16, counters, poison);
+  }
+  prof_mark(stream);
+  {
+    BwdArgs a;
+    a.lse2 = lse2;
+    a.Dvec = dvec;
+    a.dk = static_cast<__nv_bfloat16*>(dk);
+    a.dv = static_cast<__nv_bfloat16*>(dv);
+    a.tickets = tickets;
+    a.job_counter = counters;
+    a.error_flag = counters + 1;
+    a.job_begin = dt->job_begin;
+    a.tasks = dt->tasks;
+    a.B = s->batch;
+    a.N = s->seqlen;
+    a.H = s->heads;
+    a.jobs_per_head = tab->jobs;
+    a.total_jobs = total_jobs;
+    a.scale = eff_scale(s);
+    a.scale_log2 = a.scale * 1.4426950408889634f;
+    a.causal = causal ? 1 : 0;
+    a.deterministic = deterministic ? 1 : 0;
+    a.trace = g_trace;
+    a.trace_cap = g_trace_cap;
+    a.spin_bound = g_spin_bound;
+    a.split = W;
+    a.dqacc = dqacc;
+    a.n_tickets = static_cast<int>(w.n_tickets);
+    a.dump = g_dump;
+    static const int no_prefetch = [] {
+      const char* e = std::getenv("DASH_NO_PREFETCH");
+      return e ? std::atoi(e) : 0;
+    }();
+    a.prefetch =
+        (!no_prefetch && (!deterministic || (schedule == kDescending && a.split >= 4))) ? 1 : 0;
+    a.cyclic = (deterministic && schedule == kShift) ? 1 : 0;
+    a.head_group = 1;
+
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(C::NTHREADS);
+    cfg.dynamicSmemBytes = C::SMEM_BYTES;
+    cfg.stream = stream;
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, tq32, tq64, tk, tv, tdo32, tdo64, tacc, a);
+    if (le != cudaSuccess) {
+      g_last_cuda = 10000 + static_cast<int>(le);
+      return DASH_ERR_CUDA;
+    }
+  }
+  prof_mark(stream);
+  {
+    const size_t total = BN * s->heads * (D / 8);
+    const int block = 256;
+    size_t g = (total + block - 1) / block;
+    if (g > static_cast<size_t>(sms) * 16) g = static_cast<size_t>(sms) * 16;
+    dash_dq_convert_kernel<D><<<static_cast<unsigned>(g), block, 0, stream>>>(
+        dqacc, static_cast<__nv_bfloat16*>(dq), s->batch, s->seqlen, s->heads, eff_scale(s), W,
+        causal ? 1 : 0, C::TILE);
   }
   prof_mark(stream);
   return cuda_check_last();
@@ -550,6 +729,17 @@ DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const voi
   if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_AUTO) return DASH_ERR_INVALID_ARG;
   if (schedule == DASH_SCHED_AUTO) schedule = auto_schedule(s, causal);
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (tile_for(s, causal, schedule) == PairCfg::TILE) {
+    static const int pv = [] {  // experiments: pair-kernel smem plan
+      const char* e = std::getenv("DASH_PAIR_VARIANT");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (pv == 1)
+      return launch_bwd_pair<2, 2, 1>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule,
+                                      deterministic, workspace, workspace_bytes, st);
+    return launch_bwd_pair<2, 2, 2>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule,
+                                    deterministic, workspace, workspace_bytes, st);
+  }
   return s->head_dim == 128
              ? launch_bwd<128>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule,
                                deterministic, workspace, workspace_bytes, st)
@@ -595,9 +785,23 @@ DASH_API dash_status dash_attn_bwd_set_acc_split(int w) {
   return DASH_OK;
 }
 
-DASH_API size_t dash_attn_bwd_dump_bytes(const dash_shape* s) {
-  if (!shape_ok(s)) return 0;
-  return static_cast<size_t>(s->batch) * s->heads * (s->seqlen / 128) * s->seqlen * s->head_dim * 4;
+DASH_API int dash_attn_bwd_tile(const dash_shape* s, int causal, int schedule) {
+  if (!shape_ok(s) || schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_AUTO) return 0;
+  if (schedule == DASH_SCHED_AUTO) schedule = auto_schedule(s, causal);
+  return tile_for(s, causal, schedule);
+}
+
+DASH_API size_t dash_attn_bwd_dump_bytes(const dash_shape* s, int causal, int schedule) {
+  const int tile = dash_attn_bwd_tile(s, causal, schedule);
+  if (tile == 0) return 0;
+  return static_cast<size_t>(s->batch) * s->heads * (s->seqlen / tile) * s->seqlen *
+         s->head_dim * 4;
+}
+
+DASH_API dash_status dash_attn_bwd_set_tile(int tile) {
+  if (tile != 0 && tile != 128 && tile != 256) return DASH_ERR_INVALID_ARG;
+  g_tile = tile;
+  return DASH_OK;
 }
 
 DASH_API int dash_attn_bwd_resolve_schedule(const dash_shape* s, int causal, int schedule) {
@@ -612,7 +816,7 @@ DASH_API dash_status dash_attn_bwd_dump(const dash_shape* s, const void* q, cons
                                         size_t workspace_bytes, float* partials,
                                         size_t partial_bytes, void* stream) {
   if (!shape_ok(s) || !aligned16(partials)) return DASH_ERR_INVALID_ARG;
-  if (partial_bytes < dash_attn_bwd_dump_bytes(s)) return DASH_ERR_WORKSPACE;
+  if (partial_bytes < dash_attn_bwd_dump_bytes(s, causal, schedule)) return DASH_ERR_WORKSPACE;
   g_dump = partials;
   const dash_status r = dash_attn_bwd(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule,
                                       deterministic, workspace, workspace_bytes, stream);

@@ -520,3 +520,89 @@ extern "C" __attribute__((visibility("default"))) int dash_probe_tma(const void*
   if (e == cudaSuccess) e = cudaGetLastError();
   return static_cast<int>(e);
 }
+
+// Pair-MMA (cta_group::2) throughput: a cluster of two CTAs, the leader issues
+// `reps` rounds of one GEMM shape of the CTA-pair backward (bwd2.cuh) and
+// waits for completion (multicast commit).  MODE 0: M=256 N=64 K=128 SS
+// (S^T / dP^T); MODE 1: M=256 N=128 K=64 TS (dV / dK); MODE 2: M=128 N=64
+// K=256 SS, A MN-major SW128, B MN-major SW64 (dQ^T).  out[cluster] = cycles
+// per round.
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    probe_pair_mma_rate_kernel(int reps, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
+  const uint32_t cta = ptx::cluster_ctarank();
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += 128)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  ptx::fence_async_smem();
+  if (warp == 0) ptx::tmem_alloc2<512>(&tmem_base);
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbar_init();
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tb = tmem_base;
+  if (warp == 0 && cta == 0) {
+    const uint32_t s0 = ptx::smem_u32(smem);
+    const uint64_t aK = tile_desc<false>(s0, 128);
+    const uint64_t bK = tile_desc<false>(s0 + 32768, 32);
+    const uint64_t bMN = ptx::sdesc_sw128(s0 + 65536, 64 * 128, 1024);
+    const uint64_t aMN = ptx::sdesc_sw128(s0, 256 * 128, 1024);
+    const uint64_t bS64 = ptx::sdesc_sw64(s0 + 65536, 256 * 64, 512);
+    constexpr uint32_t ID0 = ptx::idesc_bf16(256, 64, 0, 0);
+    constexpr uint32_t ID1 = ptx::idesc_bf16(256, 128, 0, 1);
+    constexpr uint32_t ID2 = ptx::idesc_bf16(128, 64, 1, 1);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      if (MODE == 0) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          ptx::mma2_bf16_e(tb, aK + kstep<false>(kk, 128), bK + kstep<false>(kk, 32), ID0, 1);
+      } else if (MODE == 1) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          ptx::mma2_bf16_ts_e(tb + 128, tb + 448 + kk * 8, bMN + kstep<true>(kk, 64), ID1, 1);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk)
+          ptx::mma2_bf16_e(tb + 384, aMN + kk * 128, bS64 + kk * 64, ID2, 1);
+      }
+    }
+    ptx::mma2_commit_mc_e(&bar);
+    ptx::mbar_wait_u(&bar, 0);
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) out[blockIdx.x / 2] = (t1 - t0) / reps;
+  } else if (warp == 0) {
+    ptx::mbar_wait_u(&bar, 0);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc2<512>(tb);
+  }
+}
+
+extern "C" __attribute__((visibility("default"))) int dash_probe_pair_mma_rate(int mode, int reps,
+                                                                              int clusters,
+                                                                              long long* out) {
+  const size_t smem = 1024 + 96 * 1024;
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<2 * clusters, 128, smem>>>(reps, out);
+  };
+  if (mode == 0) launch(probe_pair_mma_rate_kernel<0>);
+  if (mode == 1) launch(probe_pair_mma_rate_kernel<1>);
+  if (mode == 2) launch(probe_pair_mma_rate_kernel<2>);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return static_cast<int>(e);
+}

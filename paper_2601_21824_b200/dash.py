@@ -64,7 +64,7 @@ def _load():
     lib.dash_attn_bwd_set_acc_split.restype = st
     lib.dash_attn_bwd_set_acc_split.argtypes = [i]
     lib.dash_attn_bwd_dump_bytes.restype = sz
-    lib.dash_attn_bwd_dump_bytes.argtypes = [SP]
+    lib.dash_attn_bwd_dump_bytes.argtypes = [SP, i, i]
     lib.dash_attn_bwd_dump.restype = st
     lib.dash_attn_bwd_dump.argtypes = [SP, vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp, sz,
                                        vp, sz, vp]
@@ -93,6 +93,10 @@ def _load():
     lib.dash_attn_bwd_set_watchdog.argtypes = [ctypes.c_longlong]
     lib.dash_attn_bwd_inject_fault.restype = st
     lib.dash_attn_bwd_inject_fault.argtypes = [i]
+    lib.dash_attn_bwd_tile.restype = i
+    lib.dash_attn_bwd_tile.argtypes = [SP, i, i]
+    lib.dash_attn_bwd_set_tile.restype = st
+    lib.dash_attn_bwd_set_tile.argtypes = [i]
     return lib
 
 
@@ -178,13 +182,13 @@ def attn_bwd(q, k, v, o, dout, lse, causal: bool, schedule=NAIVE, deterministic:
 
 def attn_bwd_trace(q, k, v, o, dout, lse, causal: bool, schedule, deterministic, trace_cap=512,
                    scale=None, workspace=None, out=None):
-    """dash_attn_bwd_trace: returns ((dq, dk, dv), trace [grid, trace_cap, 16] int64 on device)."""
+    """dash_attn_bwd_trace: returns ((dq, dk, dv), trace [grid, trace_cap, 32] int64 on device)."""
     sched = _sched(schedule)
     if workspace is None:
         workspace = alloc_workspace(q.shape, causal, sched, deterministic, q.device)
     dq, dk, dv = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)) if out is None else out
     props = torch.cuda.get_device_properties(q.device)
-    trace = torch.zeros((props.multi_processor_count, trace_cap, 16), dtype=torch.int64,
+    trace = torch.zeros((props.multi_processor_count, trace_cap, 32), dtype=torch.int64,
                         device=q.device)
     shp = _shape(q, scale)
     _check(_lib.dash_attn_bwd_trace(ctypes.byref(shp), _ptr(q), _ptr(k), _ptr(v), _ptr(o),
@@ -225,8 +229,9 @@ def attn_bwd_dump(q, k, v, o, dout, lse, causal: bool, schedule, deterministic=T
     dq, dk, dv = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)) if out is None else out
     B, N, H, d = q.shape
     shp = _shape(q, scale)
-    nbytes = int(_lib.dash_attn_bwd_dump_bytes(ctypes.byref(shp)))
-    parts = torch.zeros((B * H, N // 128, N, d), dtype=torch.float32, device=q.device)
+    nbytes = int(_lib.dash_attn_bwd_dump_bytes(ctypes.byref(shp), int(causal), sched))
+    parts = torch.zeros((B * H, N // tile(q.shape, causal, sched), N, d), dtype=torch.float32,
+                        device=q.device)
     assert parts.numel() * 4 == nbytes
     _check(_lib.dash_attn_bwd_dump(ctypes.byref(shp), _ptr(q), _ptr(k), _ptr(v), _ptr(o),
                                    _ptr(dout), _ptr(lse), _ptr(dq), _ptr(dk), _ptr(dv),
@@ -318,3 +323,16 @@ def inject_fault(poison: int):
     """dash_attn_bwd_inject_fault (verification only): the next backward on this
     thread presets its first ticket to `poison`, a value no ordered add reaches."""
     _check(_lib.dash_attn_bwd_inject_fault(int(poison)), "dash_attn_bwd_inject_fault")
+
+
+def tile(shape_bnhd, causal: bool = True, schedule="auto") -> int:
+    """dash_attn_bwd_tile: schedule tile size the backward runs with (128: the
+    single-CTA kernel, 256: the CTA-pair kernel)."""
+    B, N, H, d = shape_bnhd
+    shp = Shape(B, N, H, d, 0.0)
+    return int(_lib.dash_attn_bwd_tile(ctypes.byref(shp), int(causal), _sched(schedule)))
+
+
+def set_tile(t: int):
+    """dash_attn_bwd_set_tile: 0 = automatic, 128 forces the single-CTA kernel."""
+    _check(_lib.dash_attn_bwd_set_tile(int(t)), "dash_attn_bwd_set_tile")

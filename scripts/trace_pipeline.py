@@ -44,7 +44,7 @@ def main():
     t = tr.cpu().numpy().astype(np.int64)  # [grid, cap, 16]
     if args.npz:
         nmax = int(max(np.count_nonzero(t[c, :, 0]) for c in range(t.shape[0])))
-        np.savez_compressed(args.npz, stamps=t[:, :nmax, :16])
+        np.savez_compressed(args.npz, stamps=t[:, :nmax, :32])
     res = {"seqlen": N, "head_dim": d, "schedule": args.schedule, "causal": causal,
            "deterministic": not args.atomic}
     per = {}
@@ -52,7 +52,7 @@ def main():
         nx = int(np.count_nonzero(t[cta, :, 0]))
         if nx < 2:
             continue
-        a = t[cta, :nx, :13]
+        a = t[cta, :nx, :16]
         per.setdefault("reduce_read", []).extend((a[:, 11] - a[:, 8]).tolist())
         per.setdefault("reduce_write", []).extend((a[:, 12] - a[:, 11]).tolist())
         per.setdefault("write_to_release", []).extend((a[:, 9] - a[:, 12]).tolist())
@@ -60,6 +60,11 @@ def main():
         per.setdefault("period", []).extend(np.diff(a[:, 0]).tolist())
         per.setdefault("mma_wait_p", []).extend((a[:, 1] - a[:, 0]).tolist())
         per.setdefault("softmax", []).extend((a[:, 4] - a[:, 3]).tolist())
+        if np.count_nonzero(a[:, 15]) > 0:  # pair kernel: softmax sub-steps
+            per.setdefault("smx_to_ds_ready", []).extend((a[:, 13] - a[:, 3]).tolist())
+            per.setdefault("smx_ds_stores", []).extend((a[:, 14] - a[:, 13]).tolist())
+            per.setdefault("smx_fences", []).extend((a[:, 15] - a[:, 14]).tolist())
+            per.setdefault("smx_arrive", []).extend((a[:, 4] - a[:, 15]).tolist())
         per.setdefault("s_ready_to_smx", []).extend((a[:, 3] - a[:, 0]).tolist())
         per.setdefault("p_to_dq_issue", []).extend((a[:, 2] - a[:, 1]).tolist())
         per.setdefault("drain", []).extend((a[:, 6] - a[:, 5]).tolist())
@@ -73,7 +78,7 @@ def main():
         res[k] = {"p10": float(np.percentile(v, 10)), "p50": float(np.median(v)),
                   "p90": float(np.percentile(v, 90)), "mean": float(v.mean())}
     # raw stamps of CTA 0's first sub-tiles, relative to its first S/dP issue
-    a0 = t[0, :24, :13]
+    a0 = t[0, :24, :13]  # noqa
     base = a0[0, 0]
     res["raw_cta0"] = {SLOTS[i]: [int(v - base) if v else None for v in a0[:, i]] for i in range(13)}
     print(json.dumps({k: v for k, v in res.items() if k != "raw_cta0"}, indent=1))

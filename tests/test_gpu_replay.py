@@ -58,18 +58,19 @@ def test_dq_equals_host_resum_in_paper_order(dash, acc_split, N, d, causal, sche
 
 
 @pytest.mark.parametrize("W", [4, 8])
-@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("d,N", [(64, 2176), (128, 2176), (128, 4352)])
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("schedule", ["naive", "descending", "shift"])
-def test_replay_every_plane_live(dash, W, d, causal, schedule):
-    """n = 17 KV tiles (N = 2176): with W = 8 every accumulator plane of every
+def test_replay_every_plane_live(dash, W, d, N, causal, schedule):
+    """n = 17 KV tiles (N = 2176 with 128-row tiles; N = 4352 with the CTA-pair
+    kernel's 256-row tiles): with W = 8 every accumulator plane of every
     Q tile with >= 2W + 1 contributors receives >= 2 ordered adds (the
     ticket-order path, not just the rank-0 store); the busiest tiles
     (17 contributors) give plane 0 three adds and planes 1-7 two."""
     old = dash.acc_split()
     dash.set_acc_split(W)
     try:
-        per_plane = _replay(dash, W, 1, 2176, 1, d, causal, schedule)
+        per_plane = _replay(dash, W, 1, N, 1, d, causal, schedule)
     finally:
         dash.set_acc_split(old)
     assert all(c >= 2 for c in per_plane[:W]), per_plane
@@ -78,7 +79,7 @@ def test_replay_every_plane_live(dash, W, d, causal, schedule):
 def _replay(dash, W, B, N, H, d, causal, schedule):
     """Re-sum the dumped partials in the paper's order, compare bits; returns,
     per accumulator plane, the largest number of adds it received in one tile."""
-    T = 128                                                # schedule tile rows (AMB-11)
+    T = dash.tile((B, N, H, d), causal, schedule)  # tile rows: 128, or 256 (CTA-pair kernel)
     n = N // T
     mask = dag.CAUSAL if causal else dag.FULL
     sched = {"naive": dag.NAIVE, "descending": dag.DESCENDING, "shift": dag.SHIFT}[schedule]
@@ -87,7 +88,7 @@ def _replay(dash, W, B, N, H, d, causal, schedule):
     (dq, _, _), parts, ws = dash.attn_bwd_dump(g["q"], g["k"], g["v"], o, g["do"], lse, causal,
                                                schedule, True)
     torch.cuda.synchronize()
-    parts = parts.cpu().numpy()                                        # [B*H, N/128, N, d] fp32
+    parts = parts.cpu().numpy()                                        # [B*H, N/T, N, d] fp32
     assert dash.acc_split(N) == W                                      # AMB-27
     acc_gpu = ws[: W * B * H * N * d * 4].view(torch.float32).cpu().numpy().reshape(W, B * H, N, d)
     dq_bits = dq.view(torch.int16).cpu().numpy().view(np.uint16)     # [B, N, H, d]
@@ -137,10 +138,29 @@ def test_partials_cover_exactly_the_visited_tiles(dash):
     o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], True)
     _, parts, _ = dash.attn_bwd_dump(g["q"], g["k"], g["v"], o, g["do"], lse, True, "shift", True)
     parts = parts.cpu().numpy()[0]
-    for i in range(N // 128):
-        for j in range(N // 128):
-            blk = parts[i, j * 128:(j + 1) * 128]
+    T = dash.tile((B, N, H, d), True, "shift")
+    for i in range(N // T):
+        for j in range(N // T):
+            blk = parts[i, j * T:(j + 1) * T]
             if j >= i:
                 assert np.count_nonzero(blk) > blk.size // 2, (i, j)
             else:
                 assert not np.any(blk), (i, j)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("schedule", ["naive", "descending", "shift"])
+@pytest.mark.parametrize("W", [1, 2])
+def test_replay_single_cta_kernel_d128(dash, W, causal, schedule):
+    """d = 128 with N a multiple of 256 runs the CTA-pair kernel by default;
+    dash_attn_bwd_set_tile(128) forces the single-CTA kernel (128-row tiles),
+    whose ordered reduction is replayed here at the same shape."""
+    old_w = dash.acc_split()
+    dash.set_tile(128)
+    dash.set_acc_split(W)
+    try:
+        assert dash.tile((1, 512, 2, 128), causal, schedule) == 128
+        _replay(dash, W, 1, 512, 2, 128, causal, schedule)
+    finally:
+        dash.set_tile(0)
+        dash.set_acc_split(old_w)

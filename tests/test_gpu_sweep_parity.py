@@ -40,7 +40,8 @@ def _case(N, d, causal, seed=0):
         f = {k: v.double().numpy() for k, v in cpu.items()}
         oracle.set_threads(oracle.max_threads())
         ref = oracle.attn_bwd(f["q"], f["k"], f["v"], f["do"], causal)
-        _cache.clear()  # keep one reference in host memory at a time
+        while len(_cache) >= 2:  # bound host memory (a reference is ~1 GB)
+            _cache.pop(next(iter(_cache)))
         _cache[key] = (cpu, ref)
     return _cache[key]
 
@@ -51,9 +52,20 @@ def _nerr(x, ref):
 
 
 @pytest.mark.parametrize("N", [512, 1024])
-@pytest.mark.parametrize("d", [128, 64])
+@pytest.mark.parametrize("d,tile", [(128, 0), (128, 128), (64, 0)],
+                         ids=["d128-pair", "d128-single", "d64"])
 @pytest.mark.parametrize("causal", [True, False])
-def test_sweep_shape_every_schedule_full_tensor(dash, N, d, causal):
+def test_sweep_shape_every_schedule_full_tensor(dash, N, d, tile, causal):
+    """tile 0: the library's choice (the CTA-pair kernel with 256-row tiles at
+    d = 128); tile 128 forces the single-CTA kernel."""
+    dash.set_tile(tile)
+    try:
+        _sweep_case(dash, N, d, causal)
+    finally:
+        dash.set_tile(0)
+
+
+def _sweep_case(dash, N, d, causal):
     cpu, ref = _case(N, d, causal)
     g = {k: v.cuda() for k, v in cpu.items()}
     o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], causal)
