@@ -440,12 +440,13 @@ def sweep_rows(dash, torch, probs, causal, steps):
     rows = []
     w_bench = dash.acc_split()
     for s, g in probs:
-        row = {"seqlen": s[1], "batch": s[0], "heads": s[2], "acc_split": dash.acc_split(s[1]),
+        row = {"seqlen": s[1], "batch": s[0], "heads": s[2],
+               "acc_split": dash.acc_split(s, causal, "auto"), "tile": dash.tile(s, causal, "auto"),
                "auto": dash.resolve_schedule(s, causal, "auto")}
         f = fa_flops(*s, causal)
         cases = [("naive", "naive", True, w_bench), ("descending", "descending", True, w_bench),
                  ("shift", "shift", True, w_bench), ("atomic", "naive", False, w_bench)]
-        if dash.acc_split(s[1]) != 1:
+        if dash.acc_split(s, causal, "auto") != 1:
             cases += [("naive_w1", "naive", True, 1), ("descending_w1", "descending", True, 1),
                       ("shift_w1", "shift", True, 1)]
         # Round-robin over the cases, median per case: every schedule sees
@@ -659,7 +660,10 @@ def main():
             "config": dict(workload_config(args, world),
                            schedule_resolved={str(sh[1]): dash.resolve_schedule(sh, causal, args.schedule)
                                               for sh in full_shapes},
-                           acc_split_resolved={str(sh[1]): dash.acc_split(sh[1]) for sh in full_shapes}),
+                           acc_split_resolved={str(sh[1]): dash.acc_split(sh, causal, args.schedule)
+                                               for sh in full_shapes},
+                           tile_resolved={str(sh[1]): dash.tile(sh, causal, args.schedule)
+                                          for sh in full_shapes}),
             "frac_of_peak": value / peak / world,
             "roofline": roofline,
             "cpu_baseline": cpu,

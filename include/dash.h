@@ -89,7 +89,7 @@ dash_status dash_attn_fwd(const dash_shape* shape, const void* q, const void* k,
 
 /* Bytes of device workspace dash_attn_bwd needs for this problem: the W
  * interleaved fp32 dQ accumulators [W][B,H,N,d] (Alg.1 line 34's "dQ_i in
- * global memory"; AMB-27) -- W = dash_attn_bwd_acc_split(N) under the
+ * global memory"; AMB-27) -- W = dash_attn_bwd_acc_split(shape, ...) under the
  * current setting when deterministic != 0, W = 1 for the atomic variant --
  * D = rowsum(dO o O) and -L*log2(e) fp32 [B,H,N] (Alg.1 line 1, P:355;
  * AMB-2), one int32 ticket per (accumulator, b, h, Q sub-tile) (the "global
@@ -221,20 +221,23 @@ dash_status dash_attn_bwd_trace(const dash_shape* shape, const void* q, const vo
 int dash_attn_bwd_resolve_schedule(const dash_shape* shape, int causal, int schedule);
 
 /* Number W of interleaved fp32 dQ accumulators the deterministic backward
- * uses (AMB-27).  W = 1 is the paper's single global order per dQ tile
- * (P:395-397).  W in {2, 4, 8}: the contribution of rank k is added, in rank
- * order, into accumulator k mod W under that accumulator's own ticket, and
- * the convert kernel sums the accumulators in index order -- a fixed order,
- * so results stay bitwise deterministic, while consecutive adds into one
- * accumulator are W schedule steps apart instead of one.
- * dash_attn_bwd_acc_split(seqlen) returns the W a call with that N uses
- * (seqlen not a positive multiple of 128: returns the setting itself, 0 =
- * automatic).  The setting defaults to automatic (W = 8 for N >= 32768, 4 for
- * N >= 8192, else 2; depends on N only), or to the DASH_ACC_SPLIT environment variable.
+ * with these arguments uses (AMB-27).  W = 1 is the paper's single global
+ * order per dQ tile.  W in {2, 4, 8}: the contribution of rank k
+ * is added, in rank order, into accumulator k mod W under that accumulator's
+ * own ticket, and the convert kernel sums the accumulators in index order --
+ * a fixed order, so results stay bitwise deterministic, while consecutive
+ * adds into one accumulator are W schedule steps apart instead of one.
+ * Automatic rule (depends on N, d and the kernel only -- never on B or H, so
+ * (b, h) sharding cannot change it), with n = N / T tiles of T rows
+ * (dash_attn_bwd_tile): single-CTA kernel (T = 128): W = 8 for n >= 256, 4
+ * for n >= 64, else 2; CTA-pair kernel (T = 256): 1 for n <= 8, 2 for n <= 32,
+ * 4 for n < 128, else 8.  shape == NULL returns the setting itself (0 =
+ * automatic); an invalid shape or schedule returns 0.  The setting defaults
+ * to automatic, or to the DASH_ACC_SPLIT environment variable;
  * dash_attn_bwd_set_acc_split(w), w in {0 (automatic), 1, 2, 4, 8}, changes it
  * for later calls (host-global, not for concurrent use; other values:
  * DASH_ERR_INVALID_ARG).  The atomic variant always uses one accumulator. */
-int dash_attn_bwd_acc_split(int seqlen);
+int dash_attn_bwd_acc_split(const dash_shape* shape, int causal, int schedule);
 dash_status dash_attn_bwd_set_acc_split(int w);
 
 /* Verification variant of dash_attn_bwd (same arguments and results) that

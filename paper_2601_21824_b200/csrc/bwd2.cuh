@@ -381,6 +381,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
       ptx::mma2_commit_mc_e(&bars[P_S_FULL]);
       ptx::mma2_commit_mc_e(&bars[P_QS_EMPTY0 + st]);
     };
+    // dQ_local^T = K^T dS^T over the 256 KV rows of the pair (Alg.1 line 28):
+    // both DS buffers complete (P_DSR), the TMEM buffer drained (P_DQ_EMPTY)
+    auto issue_dq = [&](uint32_t xx) {
+      const uint32_t sb = xx % C::NDS, qb = xx & 1;
+      if (xx >= 2) ptx::mbar_wait_u(&bars[P_DQ_EMPTY0 + qb], ((xx >> 1) - 1) & 1);
+      ptx::mbar_wait_u(&bars[P_DSR0 + sb], (xx / C::NDS) & 1);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < C::TILE / 16; ++kk)
+        ptx::mma2_bf16_e(tbase + C::T_DQ + qb * 32, dKB_mn + kk * (2048 / 16),
+                         dDS + sb * DS_STEP + kk * (1024 / 16), ID_Q, kk > 0);
+      if (lane == 0) DASH_TRACE_MARK(2, xx);
+      ptx::mma2_commit_mc_e(&bars[P_DQ_FULL0 + qb]);
+      ptx::mma2_commit_mc_e(&bars[P_DS_EMPTY0 + sb]);
+    };
     while (true) {
       ptx::mbar_wait_cluster_u(&bars[P_JOB0 + (it_job & 1)], (it_job >> 1) & 1);
       const int g = __shfl_sync(0xffffffffu, job_slot[it_job & 1], 0);
@@ -439,20 +454,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
           ptx::mma2_commit_mc_e(&bars[P_DST_EMPTY]);
           ptx::mma2_commit_mc_e(&bars[P_QK_EMPTY0 + qk]);
           if (lane == 0) DASH_TRACE_MARK(16, xx);
-          // dQ_local^T = K^T dS^T over the 256 KV rows of the pair (Alg.1 line 28):
-          // both DS buffers complete (P_DSR), the TMEM buffer drained (P_DQ_EMPTY)
-          const uint32_t sb = xx % C::NDS, qb = xx & 1;
-          if (xx >= 2) ptx::mbar_wait_u(&bars[P_DQ_EMPTY0 + qb], ((xx >> 1) - 1) & 1);
-          ptx::mbar_wait_u(&bars[P_DSR0 + sb], (xx / C::NDS) & 1);
-          ptx::tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < C::TILE / 16; ++kk)
-            ptx::mma2_bf16_e(tbase + C::T_DQ + qb * 32, dKB_mn + kk * (2048 / 16),
-                             dDS + sb * DS_STEP + kk * (1024 / 16), ID_Q, kk > 0);
-          if (lane == 0) DASH_TRACE_MARK(2, xx);
-          ptx::mma2_commit_mc_e(&bars[P_DQ_FULL0 + qb]);
-          ptx::mma2_commit_mc_e(&bars[P_DS_EMPTY0 + sb]);
+          // dQ of the previous sub-tile: its dS^T exchange has had a whole
+          // sub-tile to complete, so it does not hold up S/dP of the next one
+          if (u >= 1) issue_dq(xx - 1);
         }
+        issue_dq(base + nsub - 1);
         x = base + nsub;
         ptx::mma2_commit_mc_e(&bars[P_KV_EMPTY]);
         ptx::mma2_commit_mc_e(&bars[P_ACC_FULL]);

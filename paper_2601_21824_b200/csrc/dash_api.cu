@@ -55,8 +55,13 @@ int auto_schedule(const dash_shape* s, int causal) {
 // acc_split_w8.txt): extra accumulators cost the convert kernel one more fp32
 // read each, which only pays off at long sequences.  Depends on n only, so
 // (b, h) sharding never changes it.
-int acc_split_for(int n) {
+// The CTA-pair kernel (256-row tiles, n' = N / 256 per head) measured on B200
+// (profiles/r02_acc_split_pair.txt): W = 1 -- the paper's single ordered
+// accumulator -- is fastest up to n' = 8 (its dQ partials already cover 256
+// KV rows, so the chain is short), 2 up to n' = 32, 4 below n' = 128, 8 above.
+int acc_split_for(int n, int tile = 128) {
   if (g_acc_split) return g_acc_split;
+  if (tile == 256) return n <= 8 ? 1 : n <= 32 ? 2 : n < 128 ? 4 : 8;
   return n >= 256 ? 8 : n >= 64 ? 4 : 2;
 }
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -151,8 +156,15 @@ size_t tickets_per_head(int d, int N) { return d == 128 ? 2 * (N / 64) : N / 128
 // W the backward uses: the setting (automatic: per n) when deterministic, one
 // accumulator for the atomic variant.  Resolved once per call and passed to
 // both the main kernel and the convert kernel.
-int resolved_split(const dash_shape* s, int deterministic) {
-  return deterministic ? acc_split_for(s->seqlen / 128) : 1;
+int tile_for(const dash_shape* s, int causal, int schedule);
+int auto_schedule(const dash_shape* s, int causal);
+int resolve_sched(const dash_shape* s, int causal, int schedule) {
+  return schedule == DASH_SCHED_AUTO ? auto_schedule(s, causal) : schedule;
+}
+int resolved_split(const dash_shape* s, int deterministic, int causal, int schedule) {
+  if (!deterministic) return 1;
+  const int tile = tile_for(s, causal, resolve_sched(s, causal, schedule));
+  return acc_split_for(s->seqlen / tile, tile);
 }
 
 struct WsLayout {
@@ -323,7 +335,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
                        size_t workspace_bytes, cudaStream_t stream) {
   using C = BwdCfg<D>;
   const int n = s->seqlen / 128;
-  const int W = resolved_split(s, deterministic);  // once per call: K2 and K4 agree
+  const int W = resolved_split(s, deterministic, causal, schedule);  // once: K2 and K4 agree
   const WsLayout w = ws_layout(s, W);
   // The setting may have changed since the workspace was sized.
   if (workspace_bytes < w.total) return DASH_ERR_WORKSPACE;
@@ -489,7 +501,7 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
   using C = PairCfgT<NQS, NQK, NDS>;
   constexpr int D = 128;
   const int n = s->seqlen / C::TILE;
-  const int W = resolved_split(s, deterministic);
+  const int W = resolved_split(s, deterministic, causal, schedule);
   const WsLayout w = ws_layout(s, W);
   if (workspace_bytes < w.total) return DASH_ERR_WORKSPACE;
   const ScheduleTable* tab = cached_schedule(schedule, n, causal ? kCausal : kFull);
@@ -711,10 +723,9 @@ DASH_API dash_status dash_attn_fwd(const dash_shape* s, const void* q, const voi
 
 DASH_API size_t dash_attn_bwd_workspace_bytes(const dash_shape* s, int causal, int schedule,
                                               int deterministic) {
-  (void)causal;
-  (void)schedule;
   if (!shape_ok(s)) return 0;
-  return ws_layout(s, resolved_split(s, deterministic)).total;
+  if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_AUTO) return 0;
+  return ws_layout(s, resolved_split(s, deterministic, causal, schedule)).total;
 }
 
 DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const void* k, const void* v,
@@ -774,9 +785,10 @@ DASH_API dash_status dash_attn_bwd_trace(const dash_shape* s, const void* q, con
   return r;
 }
 
-DASH_API int dash_attn_bwd_acc_split(int seqlen) {
-  if (seqlen < 128 || seqlen % 128) return acc_split();
-  return acc_split_for(seqlen / 128);
+DASH_API int dash_attn_bwd_acc_split(const dash_shape* s, int causal, int schedule) {
+  if (!s) return acc_split();
+  if (!shape_ok(s) || schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_AUTO) return 0;
+  return resolved_split(s, 1, causal, schedule);
 }
 
 DASH_API dash_status dash_attn_bwd_set_acc_split(int w) {
@@ -847,7 +859,7 @@ struct HostPlan {
   size_t in_bytes, lse_bytes;  // per chunk (largest)
   size_t q, k, v, o, dout, lse, dq, dk, dv, inner, slot, total;
 };
-HostPlan host_plan(const dash_shape* s, int deterministic) {
+HostPlan host_plan(const dash_shape* s, int causal, int schedule, int deterministic) {
   HostPlan h;
   const int kc = host_chunks();
   if (s->batch >= kc) {
@@ -874,7 +886,8 @@ HostPlan host_plan(const dash_shape* s, int deterministic) {
   h.lse = off;
   off = align_up(off + h.lse_bytes, kAlign);
   h.inner = off;
-  h.slot = align_up(off + ws_layout(&cs, resolved_split(&cs, deterministic)).total, kAlign);
+  h.slot = align_up(off + ws_layout(&cs, resolved_split(&cs, deterministic, causal, schedule)).total,
+                    kAlign);
   h.total = kHostSlots * h.slot;
   return h;
 }
@@ -925,10 +938,9 @@ cudaError_t copy_chunk(void* dst, const void* src, const dash_shape* s, int b0, 
 
 DASH_API size_t dash_attn_bwd_host_workspace_bytes(const dash_shape* s, int causal, int schedule,
                                                    int deterministic) {
-  (void)causal;
-  (void)schedule;
   if (!shape_ok(s)) return 0;
-  return host_plan(s, deterministic).total;
+  if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_AUTO) return 0;
+  return host_plan(s, causal, schedule, deterministic).total;
 }
 
 DASH_API dash_status dash_attn_bwd_host(const dash_shape* s, const void* q, const void* k,
@@ -942,7 +954,8 @@ DASH_API dash_status dash_attn_bwd_host(const dash_shape* s, const void* q, cons
   for (const void* p : hptrs)
     if (!p) return DASH_ERR_INVALID_ARG;
   if (!aligned16(workspace)) return DASH_ERR_INVALID_ARG;
-  const HostPlan h = host_plan(s, deterministic);
+  if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_AUTO) return DASH_ERR_INVALID_ARG;
+  const HostPlan h = host_plan(s, causal, schedule, deterministic);
   if (workspace_bytes < h.total) return DASH_ERR_WORKSPACE;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return DASH_ERR_CUDA;
@@ -1004,10 +1017,9 @@ DASH_API dash_status dash_attn_bwd_host(const dash_shape* s, const void* q, cons
 
 DASH_API dash_status dash_check_workspace(const dash_shape* s, int causal, int schedule,
                                           int deterministic, const void* workspace, void* stream) {
-  (void)causal;
-  (void)schedule;
   if (!shape_ok(s) || !workspace) return DASH_ERR_INVALID_ARG;
-  const WsLayout w = ws_layout(s, resolved_split(s, deterministic));
+  if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_AUTO) return DASH_ERR_INVALID_ARG;
+  const WsLayout w = ws_layout(s, resolved_split(s, deterministic, causal, schedule));
   int flag = 0;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   int* dflag = reinterpret_cast<int*>(static_cast<char*>(const_cast<void*>(workspace)) + w.counters) + 1;

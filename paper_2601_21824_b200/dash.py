@@ -60,7 +60,7 @@ def _load():
     lib.dash_attn_bwd_resolve_schedule.restype = i
     lib.dash_attn_bwd_resolve_schedule.argtypes = [SP, i, i]
     lib.dash_attn_bwd_acc_split.restype = i
-    lib.dash_attn_bwd_acc_split.argtypes = [i]
+    lib.dash_attn_bwd_acc_split.argtypes = [SP, i, i]
     lib.dash_attn_bwd_set_acc_split.restype = st
     lib.dash_attn_bwd_set_acc_split.argtypes = [i]
     lib.dash_attn_bwd_dump_bytes.restype = sz
@@ -209,10 +209,14 @@ def resolve_schedule(shape_bnhd, causal: bool, schedule) -> str:
     return {NAIVE: "naive", DESCENDING: "descending", SHIFT: "shift"}[r]
 
 
-def acc_split(seqlen: int = 0) -> int:
-    """dash_attn_bwd_acc_split: the W a call with this seqlen uses (AMB-27);
-    seqlen = 0 returns the setting (0 = automatic)."""
-    return int(_lib.dash_attn_bwd_acc_split(int(seqlen)))
+def acc_split(shape_bnhd=None, causal: bool = True, schedule="auto") -> int:
+    """dash_attn_bwd_acc_split: the W a deterministic backward with this shape
+    uses (AMB-27); shape None returns the setting (0 = automatic)."""
+    if shape_bnhd is None:
+        return int(_lib.dash_attn_bwd_acc_split(None, 0, 0))
+    B, N, H, d = shape_bnhd
+    shp = Shape(B, N, H, d, 0.0)
+    return int(_lib.dash_attn_bwd_acc_split(ctypes.byref(shp), int(causal), _sched(schedule)))
 
 
 def set_acc_split(w: int):

@@ -32,7 +32,7 @@ def main():
     out = tuple(torch.empty_like(g["q"]) for _ in range(3))
     flops = 10.0 * B * H * N * N * d / 2
     res = {"config": "long-context", "B": B, "N": N, "H": H, "d": d, "mask": "causal",
-           "flops_fa_convention": flops, "acc_split": dash.acc_split(N),
+           "flops_fa_convention": flops, "acc_split": dash.acc_split((B, N, H, d), True),
            "auto_schedule": dash.resolve_schedule((B, N, H, d), True, "auto")}
     for name, sched, det in (("naive", "naive", True), ("descending", "descending", True),
                              ("shift", "shift", True), ("atomic", "naive", False),

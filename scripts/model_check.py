@@ -70,6 +70,7 @@ def main():
                     help="W (AMB-27); the DAG model is the paper's single chain, W = 1")
     args = ap.parse_args()
     dash.set_acc_split(args.acc_split)
+    dash.set_tile(128)  # the DAG model below is one SM per 128-row KV tile
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     rows = []
     for n in (int(v) for v in args.ns.split(",")):
@@ -83,7 +84,7 @@ def main():
             mask = dash.CAUSAL if causal else dash.FULL
             m = B * H
             row = {"n": n, "N": N, "B": B, "H": H, "mask": "causal" if causal else "full",
-                   "acc_split": dash.acc_split(N),
+                   "acc_split": dash.acc_split((B, N, H, d), causal),
                    "c_cycles": c, "r_cycles": r, "n_sm": sms, "heads_m": m}
             t_naive = time_bwd(g, causal, "naive")
             cp_naive = dash.schedule_critical_path(dash.NAIVE, n, n, mask, m, sms, c, r)

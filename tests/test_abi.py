@@ -156,10 +156,16 @@ def test_auto_schedule_policy_and_acc_split(dash):
     old = dash.acc_split()
     try:
         dash.set_acc_split(0)
-        assert [dash.acc_split(N) for N in (512, 4096, 8192, 16384, 32768)] == [2, 2, 4, 4, 8]
+        # single-CTA kernel (d = 64, 128-row tiles): n = N / 128
+        assert [dash.acc_split((1, N, 16, 64), True) for N in (512, 4096, 8192, 16384, 32768)] == \
+            [2, 2, 4, 4, 8]
+        # CTA-pair kernel (d = 128, 256-row tiles): n = N / 256
+        assert [dash.acc_split((1, N, 16, 128), True) for N in (512, 2048, 4096, 8192, 16384, 32768)] == \
+            [1, 1, 2, 2, 4, 8]
+        assert dash.acc_split((1, 8192, 16, 128), True) == dash.acc_split((8, 8192, 32, 128), True)
         for w in (1, 2, 4, 8):
             dash.set_acc_split(w)
-            assert dash.acc_split(1024) == w and dash.acc_split() == w
+            assert dash.acc_split((1, 1024, 2, 128), False) == w and dash.acc_split() == w
         with pytest.raises(dash.DashError):
             dash.set_acc_split(3)
     finally:

@@ -89,7 +89,7 @@ def _replay(dash, W, B, N, H, d, causal, schedule):
                                                schedule, True)
     torch.cuda.synchronize()
     parts = parts.cpu().numpy()                                        # [B*H, N/T, N, d] fp32
-    assert dash.acc_split(N) == W                                      # AMB-27
+    assert dash.acc_split((B, N, H, d), causal, schedule) == W         # AMB-27
     acc_gpu = ws[: W * B * H * N * d * 4].view(torch.float32).cpu().numpy().reshape(W, B * H, N, d)
     dq_bits = dq.view(torch.int16).cpu().numpy().view(np.uint16)     # [B, N, H, d]
     scale = np.float32(1.0) / np.sqrt(np.float32(d))

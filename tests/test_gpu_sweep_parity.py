@@ -87,7 +87,7 @@ def test_d64_long_sequence_sampled_rows(dash, causal):
     B, N, H, d = sweep_shape(16384, 64)
     cpu = attn_inputs(B, N, H, d, seed=2)
     g = {k: v.cuda() for k, v in cpu.items()}
-    assert dash.acc_split(N) == 4
+    assert dash.acc_split((B, N, H, d), causal, "auto") == 4
     o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], causal)
     dq, dk, dv = dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal, "auto", True)
     torch.cuda.synchronize()
