@@ -230,7 +230,7 @@ int dash_attn_bwd_resolve_schedule(const dash_shape* shape, int causal, int sche
  * Automatic rule (depends on N, d and the kernel only -- never on B or H, so
  * (b, h) sharding cannot change it), with n = N / T tiles of T rows
  * (dash_attn_bwd_tile): single-CTA kernel (T = 128): W = 8 for n >= 256, 4
- * for n >= 64, else 2; CTA-pair kernel (T = 256): 1 for n <= 8, 2 for n <= 32,
+ * for n >= 64, else 2; CTA-pair kernel (T = 256): 1 for n <= 8, 2 for n <= 16,
  * 4 for n < 128, else 8.  shape == NULL returns the setting itself (0 =
  * automatic); an invalid shape or schedule returns 0.  The setting defaults
  * to automatic, or to the DASH_ACC_SPLIT environment variable;

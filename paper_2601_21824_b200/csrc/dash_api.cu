@@ -58,10 +58,10 @@ int auto_schedule(const dash_shape* s, int causal) {
 // The CTA-pair kernel (256-row tiles, n' = N / 256 per head) measured on B200
 // (profiles/r02_acc_split_pair.txt): W = 1 -- the paper's single ordered
 // accumulator -- is fastest up to n' = 8 (its dQ partials already cover 256
-// KV rows, so the chain is short), 2 up to n' = 32, 4 below n' = 128, 8 above.
+// KV rows, so the chain is short), 2 up to n' = 16, 4 below n' = 128, 8 above.
 int acc_split_for(int n, int tile = 128) {
   if (g_acc_split) return g_acc_split;
-  if (tile == 256) return n <= 8 ? 1 : n <= 32 ? 2 : n < 128 ? 4 : 8;
+  if (tile == 256) return n <= 8 ? 1 : n <= 16 ? 2 : n < 128 ? 4 : 8;
   return n >= 256 ? 8 : n >= 64 ? 4 : 2;
 }
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }

@@ -161,7 +161,7 @@ def test_auto_schedule_policy_and_acc_split(dash):
             [2, 2, 4, 4, 8]
         # CTA-pair kernel (d = 128, 256-row tiles): n = N / 256
         assert [dash.acc_split((1, N, 16, 128), True) for N in (512, 2048, 4096, 8192, 16384, 32768)] == \
-            [1, 1, 2, 2, 4, 8]
+            [1, 1, 2, 4, 4, 8]
         assert dash.acc_split((1, 8192, 16, 128), True) == dash.acc_split((8, 8192, 32, 128), True)
         for w in (1, 2, 4, 8):
             dash.set_acc_split(w)
