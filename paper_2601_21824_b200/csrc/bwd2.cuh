@@ -435,23 +435,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
           // S/dP of the next sub-tile go into the tensor pipe while the softmax
           // warps turn this one into P^T / dS^T (dQ is issued by the drain).
           if (u + 1 < nsub) issue_sdp(xx + 1);
+          // QK operands first (normally long loaded), so the reaction to
+          // P_FULL is only the MMA issue
+          ptx::mbar_wait_u(&bars[P_QK_FULL0 + qk], (xx / NQK) & 1);
+          if (u == 0 && acc_cnt > 0) ptx::mbar_wait_u(&bars[P_ACC_EMPTY], (acc_cnt - 1) & 1);
           ptx::mbar_wait_u(&bars[P_P_FULL], xx & 1);
           if (lane == 0) DASH_TRACE_MARK(1, xx);
-          if (u == 0 && acc_cnt > 0) ptx::mbar_wait_u(&bars[P_ACC_EMPTY], (acc_cnt - 1) & 1);
-          ptx::mbar_wait_u(&bars[P_QK_FULL0 + qk], (xx / NQK) & 1);
           ptx::tc_fence_after();
+          // dK += dS^T Q   (Alg.1 line 26) -- first: the softmax of the next
+          // sub-tile writes its dS^T into this TMEM buffer first
+#pragma unroll
+          for (int kk = 0; kk < BR / 16; ++kk)
+            ptx::mma2_bf16_ts_e(tbase + C::T_DK, tbase + C::T_DST + kk * 8,
+                                dQK + qk * ST_STEP + kstep<true>(kk, BR), ID_KV, (u > 0 || kk > 0));
+          ptx::mma2_commit_mc_e(&bars[P_DST_EMPTY]);
           // dV += P^T dO   (Alg.1 line 25)
 #pragma unroll
           for (int kk = 0; kk < BR / 16; ++kk)
             ptx::mma2_bf16_ts_e(tbase + C::T_DV, tbase + C::T_PT + kk * 8,
                                 dDOK + qk * ST_STEP + kstep<true>(kk, BR), ID_KV, (u > 0 || kk > 0));
           ptx::mma2_commit_mc_e(&bars[P_PT_EMPTY]);
-          // dK += dS^T Q   (Alg.1 line 26)
-#pragma unroll
-          for (int kk = 0; kk < BR / 16; ++kk)
-            ptx::mma2_bf16_ts_e(tbase + C::T_DK, tbase + C::T_DST + kk * 8,
-                                dQK + qk * ST_STEP + kstep<true>(kk, BR), ID_KV, (u > 0 || kk > 0));
-          ptx::mma2_commit_mc_e(&bars[P_DST_EMPTY]);
           ptx::mma2_commit_mc_e(&bars[P_QK_EMPTY0 + qk]);
           if (lane == 0) DASH_TRACE_MARK(16, xx);
           // dQ of the previous sub-tile: its dS^T exchange has had a whole
@@ -635,10 +638,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
           else smx(std::false_type{});
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&bars[P_LD_EMPTY0 + st]);  // L, D of this slot read
-          if (x >= 1) ptx::mbar_wait(&bars[P_PT_EMPTY], (x - 1) & 1);
-          ptx::tmem_st16(tbase + lane_off + C::T_PT + cc0 / 2, pk);
           if (x >= 1) ptx::mbar_wait(&bars[P_DST_EMPTY], (x - 1) & 1);
           ptx::tmem_st16(tbase + lane_off + C::T_DST + cc0 / 2, dk2);
+          if (x >= 1) ptx::mbar_wait(&bars[P_PT_EMPTY], (x - 1) & 1);
+          ptx::tmem_st16(tbase + lane_off + C::T_PT + cc0 / 2, pk);
           ptx::tmem_wait_st();
           ptx::tc_fence_before();
           __syncwarp();
