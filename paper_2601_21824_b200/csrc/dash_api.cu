@@ -740,17 +740,9 @@ DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const voi
   if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_AUTO) return DASH_ERR_INVALID_ARG;
   if (schedule == DASH_SCHED_AUTO) schedule = auto_schedule(s, causal);
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (tile_for(s, causal, schedule) == PairCfg::TILE) {
-    static const int pv = [] {  // experiments: pair-kernel smem plan
-      const char* e = std::getenv("DASH_PAIR_VARIANT");
-      return e ? std::atoi(e) : 0;
-    }();
-    if (pv == 1)
-      return launch_bwd_pair<2, 2, 1>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule,
-                                      deterministic, workspace, workspace_bytes, st);
+  if (tile_for(s, causal, schedule) == PairCfg::TILE)
     return launch_bwd_pair<2, 2, 2>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule,
                                     deterministic, workspace, workspace_bytes, st);
-  }
   return s->head_dim == 128
              ? launch_bwd<128>(s, q, k, v, o, dout, lse, dq, dk, dv, causal, schedule,
                                deterministic, workspace, workspace_bytes, st)

@@ -569,7 +569,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           ptx::mma2_bf16_ts_e(tb + 128, tb + 448 + kk * 8, bMN + kstep<true>(kk, 64), ID1, 1);
+      } else if (MODE == 2) {
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk)
+          ptx::mma2_bf16_e(tb + 384, aMN + kk * 128, bS64 + kk * 64, ID2, 1);
       } else {
+        // MODE 3: one sub-tile of the pair kernel in its issue order:
+        // S^T, dP^T (SS), dK, dV (TS), dQ^T (SS, M = 128)
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          ptx::mma2_bf16_e(tb, aK + kstep<false>(kk, 128), bK + kstep<false>(kk, 32), ID0, 1);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          ptx::mma2_bf16_e(tb + 64, aK + kstep<false>(kk, 128), bK + kstep<false>(kk, 32), ID0, 1);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          ptx::mma2_bf16_ts_e(tb + 256, tb + 480 + kk * 8, bMN + kstep<true>(kk, 64), ID1, 1);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          ptx::mma2_bf16_ts_e(tb + 128, tb + 448 + kk * 8, bMN + kstep<true>(kk, 64), ID1, 1);
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk)
           ptx::mma2_bf16_e(tb + 384, aMN + kk * 128, bS64 + kk * 64, ID2, 1);
@@ -602,6 +620,7 @@ extern "C" __attribute__((visibility("default"))) int dash_probe_pair_mma_rate(i
   if (mode == 0) launch(probe_pair_mma_rate_kernel<0>);
   if (mode == 1) launch(probe_pair_mma_rate_kernel<1>);
   if (mode == 2) launch(probe_pair_mma_rate_kernel<2>);
+  if (mode == 3) launch(probe_pair_mma_rate_kernel<3>);
   cudaError_t e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = cudaGetLastError();
   return static_cast<int>(e);

@@ -15,7 +15,7 @@ h = rows[0]
 per = {}
 for r in rows[1:]:
     d = dict(zip(h, r))
-    if "dash_bwd_kernel" not in d["Kernel Name"]:
+    if "dash_bwd_kernel" not in d["Kernel Name"] and "dash_bwd_pair_kernel" not in d["Kernel Name"]:
         continue
     per.setdefault(d["ID"], {})[d["Metric Name"]] = float(d["Metric Value"])
 launches = [v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for v in per.values()]

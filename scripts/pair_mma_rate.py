@@ -9,7 +9,8 @@ lib = ctypes.CDLL(os.path.join(ROOT, "paper_2601_21824_b200", "libdash_probe.so"
 lib.dash_probe_pair_mma_rate.argtypes = [ctypes.c_int] * 3 + [ctypes.c_void_p]
 shapes = {0: ("S^T/dP^T M=256 N=64 K=128 SS", 256 * 64 * 128),
           1: ("dV/dK M=256 N=128 K=64 TS", 256 * 128 * 64),
-          2: ("dQ^T M=128 N=64 K=256 SS (B SW64)", 128 * 64 * 256)}
+          2: ("dQ^T M=128 N=64 K=256 SS (B SW64)", 128 * 64 * 256),
+          3: ("one sub-tile: S,dP,dK,dV,dQ (pair)", 2 * 256 * 64 * 128 + 2 * 256 * 128 * 64 + 128 * 64 * 256)}
 for clusters in (1, 74):
     for mode, (name, macs) in shapes.items():
         out = torch.zeros(clusters, dtype=torch.int64, device="cuda")
