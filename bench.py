@@ -581,8 +581,10 @@ def main():
     achieved = rank_tile * args.steps / (ms_main_timed / 1e3) / 1e12
     wl = workload_config(args, world)["workload"]
     traffic = load_traffic(wl)
+    tiles = {dash.tile(g["shape"], causal, args.schedule) for _, g in probs}
+    main_kernel = "+".join(sorted({256: "dash_bwd_pair_kernel", 128: "dash_bwd_kernel"}[t] for t in tiles))
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": traffic, "kernel": "dash_bwd_kernel",
+                "frac": achieved / peak, "traffic": traffic, "kernel": main_kernel,
                 "peak_source": peak_src,
                 "frac_vs_sustained": achieved / peak_sus if peak_sus else None,
                 "main_kernel_share_of_step": ms_main_timed / ms if ms > 0 else None}

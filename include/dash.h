@@ -285,8 +285,25 @@ int dash_attn_bwd_tile(const dash_shape* shape, int causal, int schedule);
  * environment sets the initial value. */
 dash_status dash_attn_bwd_set_tile(int tile);
 
+/* dQ-plane budget.  The W fp32 dQ accumulators (AMB-27) of all B*H heads take
+ * W * B*H*N*d*4 bytes of the workspace -- 32 GiB at BASELINE config 4 (B = 8,
+ * H = 32, N = 32k, d = 128, W = 8).  When that exceeds the budget (default 4
+ * GiB), dash_attn_bwd processes the flattened heads in chunks of
+ * dash_attn_bwd_head_chunk(...) consecutive heads (main kernel + dQ convert
+ * per chunk, one preprocess) that reuse one set of accumulator planes, and
+ * dash_attn_bwd_workspace_bytes shrinks accordingly.  A chunk is a (b, h)
+ * shard (heads are independent, §2.1): every per-head schedule, rank and
+ * accumulation order is unchanged, so results are bit-identical for every
+ * budget.  set_plane_budget(0) restores the default; host-global, applies to
+ * later calls (a workspace sized under another budget may then be too small:
+ * DASH_ERR_WORKSPACE).  head_chunk returns the heads per chunk (B*H when one
+ * chunk suffices), 0 for an invalid shape or schedule. */
+dash_status dash_attn_bwd_set_plane_budget(size_t bytes);
+int dash_attn_bwd_head_chunk(const dash_shape* shape, int causal, int schedule, int deterministic);
+
 /* Number of device kernel launches one dash_attn_bwd makes (for accounting):
- * 3 (preprocess, main, dQ convert). */
+ * 3 (preprocess, main, dQ convert) when the heads fit one chunk (see
+ * dash_attn_bwd_head_chunk), else 1 + 2 * chunks. */
 int dash_attn_bwd_launches(int causal, int schedule, int deterministic);
 
 /* Diagnostic code behind the calling thread's most recent DASH_ERR_CUDA (0 if

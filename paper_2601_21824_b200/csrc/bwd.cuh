@@ -78,6 +78,13 @@ struct BwdArgs {
   // orders and reduction ranks are unchanged, so results are bit-identical
   // for every G; G only amortises the per-job claim / drain cost.
   int head_group;
+  // Head chunk of this launch (dQ-plane budget, dash_attn_bwd_set_plane_budget):
+  // jobs cover the flattened heads bh_base .. bh_base + bh_count - 1; the W
+  // accumulators and ticket sets hold only those heads (local index
+  // bh - bh_base, plane stride bh_count).  One launch = one chunk = B*H heads
+  // unless the planes of all heads exceed the budget.
+  int bh_base;
+  int bh_count;
 };
 
 // Per-(CTA, sub-tile) clock64 stamps for pipeline analysis; a null trace
@@ -209,7 +216,7 @@ struct JobView {
 };
 __device__ __forceinline__ JobView decode_job(const BwdArgs& a, int g) {
   JobView j;
-  j.bh0 = (g / a.jobs_per_head) * a.head_group;
+  j.bh0 = a.bh_base + (g / a.jobs_per_head) * a.head_group;
   const int lj = g % a.jobs_per_head;
   j.t0 = a.job_begin[lj];
   j.t1 = a.job_begin[lj + 1];
@@ -522,7 +529,7 @@ __global__ void __launch_bounds__(512, 1)
             const int urow = q * 128 + sub * BR;  // first Q row of the unit
             const int par = rank % args.split, rank_w = rank / args.split;  // AMB-27
             int* ticket = args.tickets + static_cast<size_t>(par) * args.n_tickets +
-                          static_cast<size_t>(tv.bh) * n_units + urow / C::STG_ROWS;
+                          static_cast<size_t>(tv.bh - args.bh_base) * n_units + urow / C::STG_ROWS;
             if (det) {
               // Wait until the global order grants this block its turn (Alg.1 line 33).
               // Spin with relaxed loads (an acquire per poll would invalidate L1
@@ -547,7 +554,7 @@ __global__ void __launch_bounds__(512, 1)
             DASH_TRACE_MARK(7, x);
             // Add dQ_local to dQ (Alg.1 line 34); rank 0 stores (no zero-fill needed).
             // row of dQacc [W][B*H*N, D]
-            const int grow = (par * args.B * args.H + tv.bh) * args.N + urow;
+            const int grow = (par * args.bh_count + tv.bh - args.bh_base) * args.N + urow;
             if constexpr (C::LINEAR) {
               // NPART parts, each reduced as soon as the drain has written it;
               // a part is handed back as soon as the bulk engine has read it
@@ -900,17 +907,17 @@ __global__ void dash_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
 // has j + 1).
 template <int D>
 __global__ void dash_dq_convert_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq,
-                                       int B, int N, int H, float scale, int split, int causal,
-                                       int tile) {
+                                       int N, int H, float scale, int split, int causal,
+                                       int tile, int bh_base, int bh_count) {
   constexpr int T = D / 8;
-  const size_t total = static_cast<size_t>(B) * H * N * T;
-  const size_t plane = static_cast<size_t>(B) * H * N * D;
+  const size_t total = static_cast<size_t>(bh_count) * N * T;
+  const size_t plane = static_cast<size_t>(bh_count) * N * D;
   for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const int part = static_cast<int>(i % T);
-    const size_t r = i / T;  // (b*H + h)*N + n
+    const size_t r = i / T;  // (local head)*N + n
     const int n = static_cast<int>(r % N);
-    const size_t bh = r / N;
+    const size_t bh = bh_base + r / N;
     const int h = static_cast<int>(bh % H);
     const int b = static_cast<int>(bh / H);
     float4 x0 = *reinterpret_cast<const float4*>(acc + r * D + part * 8);

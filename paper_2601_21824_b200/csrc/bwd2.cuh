@@ -126,7 +126,7 @@ enum : int {
   P_LD_FULL0 = 22,               // (B) + slot (NLD = 3): this CTA's L/D loaded (1 + tx)
   P_QS_EMPTY0 = 25,              // (B) + slot: consumed by S^T / dP^T (commit)
   P_QK_EMPTY0 = 28,              // (B) + slot: consumed by dV / dK (commit)
-  P_LD_EMPTY0 = 30,              // (B) + slot: L/D read by this CTA's softmax (8 warps)
+  P_LD_EMPTY0 = 30,              // (B) + slot: L/D read by this CTA's softmax (256 threads)
   P_DS_EMPTY0 = 33,              // (B) + buf: dS^T smem consumed by dQ (commit)
   P_PF0 = 35,                    // (L) + (t-1)%2: producer's claim decision (1)
   P_SLOT_FREE0 = 37,             // (L) + j%2: all 32 warps of the pair read job j's slot (32)
@@ -180,7 +180,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
     ptx::mbar_init(&bars[P_SLOT_FREE0], 32);
     ptx::mbar_init(&bars[P_SLOT_FREE0 + 1], 32);
     for (int i = 0; i < 2 * NAG; ++i) ptx::mbar_init(&bars[P_AGF0 + i], 64);
-    for (int i = 0; i < C::NLD; ++i) ptx::mbar_init(&bars[P_LD_EMPTY0 + i], 8);
+    for (int i = 0; i < C::NLD; ++i) ptx::mbar_init(&bars[P_LD_EMPTY0 + i], 256);
     for (int i = 0; i < 2; ++i) ptx::mbar_init(&bars[P_DSR0 + i], leader ? 5 : 4);
 
     ptx::fence_mbar_init();
@@ -501,7 +501,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
             const int urow = q * C::TILE + sub * BR;  // first Q row of the unit
             const int par = rank % args.split, rank_w = rank / args.split;  // AMB-27
             int* ticket = args.tickets + static_cast<size_t>(par) * args.n_tickets +
-                          (static_cast<size_t>(tv.bh) * n_units + urow / BR) * 2 + cta;
+                          (static_cast<size_t>(tv.bh - args.bh_base) * n_units + urow / BR) * 2 + cta;
             if (det) {
               if (ptx::ld_acquire(ticket) != rank_w) {
                 const long long t_start = clock64();
@@ -521,7 +521,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
             }
             DASH_TRACE_MARK(7, x);
             // Add this CTA's d half of dQ_local into dQ (Alg.1 line 34); rank 0 stores.
-            const int grow = (par * args.B * args.H + tv.bh) * args.N + urow;
+            const int grow = (par * args.bh_count + tv.bh - args.bh_base) * args.N + urow;
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
               ptx::mbar_wait(&bars[P_AGF0 + hh * NAG + agent], ph);
@@ -636,8 +636,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
           };
           if (diag) smx(std::true_type{});
           else smx(std::false_type{});
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&bars[P_LD_EMPTY0 + st]);  // L, D of this slot read
+          ptx::mbar_arrive(&bars[P_LD_EMPTY0 + st]);  // this thread's L, D reads of the slot are done
           if (x >= 1) ptx::mbar_wait(&bars[P_DST_EMPTY], (x - 1) & 1);
           ptx::tmem_st16(tbase + lane_off + C::T_DST + cc0 / 2, dk2);
           if (x >= 1) ptx::mbar_wait(&bars[P_PT_EMPTY], (x - 1) & 1);

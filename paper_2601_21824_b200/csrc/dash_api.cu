@@ -167,20 +167,40 @@ int resolved_split(const dash_shape* s, int deterministic, int causal, int sched
   return acc_split_for(s->seqlen / tile, tile);
 }
 
+// dQ-plane budget (dash_attn_bwd_set_plane_budget): the W fp32 accumulators
+// of all B*H heads take W * B*H*N*d*4 bytes -- 32 GiB at config 4 (B = 8,
+// H = 32, N = 32k, d = 128, W = 8).  When that exceeds the budget the heads
+// are processed in chunks of `chunk` consecutive flattened heads that reuse
+// one set of planes (BwdArgs::bh_base / bh_count).  A chunk is a (b, h) shard:
+// the per-head schedules, ranks and accumulation order are unchanged, so the
+// results are bit-identical for every budget.
+constexpr size_t kDefaultPlaneBudget = size_t(4) << 30;
+size_t g_plane_budget = kDefaultPlaneBudget;
+
 struct WsLayout {
   size_t dqacc = 0, dvec = 0, lse2 = 0, tickets = 0, counters = 0, total = 0;
-  size_t dqacc_bytes = 0, n_tickets = 0;
+  size_t dqacc_bytes = 0, n_tickets = 0;  // per accumulator, for one chunk of heads
   int planes = 1;
+  int chunk = 1, chunks = 1;  // heads per chunk, number of chunks
 };
 // W interleaved fp32 accumulators (AMB-27), each with its own ticket set:
-// dqacc [W][B,H,N,d], tickets [W][B*H][N / ticket_rows].  The accumulators
-// come first (offset 0), so a verification test can read them back.
-WsLayout ws_layout(const dash_shape* s, int W) {
+// dqacc [W][chunk heads, N, d], tickets [W][chunk heads][N / ticket_rows]; D
+// and -L*log2(e) for all heads.  The accumulators come first (offset 0), so a
+// verification test can read them back.  `G` = head grouping (chunks are
+// multiples of it).
+WsLayout ws_layout(const dash_shape* s, int W, int G = 1) {
   WsLayout w;
   w.planes = W;
-  const size_t BHN = static_cast<size_t>(s->batch) * s->heads * s->seqlen;
-  w.dqacc_bytes = BHN * s->head_dim * 4;
-  w.n_tickets = static_cast<size_t>(s->batch) * s->heads * tickets_per_head(s->head_dim, s->seqlen);
+  const int BH = s->batch * s->heads;
+  const size_t per_head = static_cast<size_t>(W) * s->seqlen * s->head_dim * 4;
+  size_t c = g_plane_budget / per_head;
+  c = c / G * G;
+  if (c < static_cast<size_t>(G)) c = G;
+  w.chunk = c >= static_cast<size_t>(BH) ? BH : static_cast<int>(c);
+  w.chunks = (BH + w.chunk - 1) / w.chunk;
+  const size_t BHN = static_cast<size_t>(BH) * s->seqlen;
+  w.dqacc_bytes = static_cast<size_t>(w.chunk) * s->seqlen * s->head_dim * 4;
+  w.n_tickets = static_cast<size_t>(w.chunk) * tickets_per_head(s->head_dim, s->seqlen);
   size_t off = 0;
   w.dqacc = off;
   off = align_up(off + static_cast<size_t>(W) * w.dqacc_bytes, kAlign);
@@ -190,10 +210,17 @@ WsLayout ws_layout(const dash_shape* s, int W) {
   off = align_up(off + BHN * 4, kAlign);
   w.tickets = off;
   off = align_up(off + static_cast<size_t>(W) * w.n_tickets * 4, kAlign);
-  w.counters = off;  // [0] job counter, [1] error flag
+  w.counters = off;  // [0] job counter, [1] error flag (directly after the tickets)
   off = align_up(off + 64, kAlign);
   w.total = off;
   return w;
+}
+
+// The layout a call with these arguments uses (schedule may be AUTO).
+WsLayout layout_for(const dash_shape* s, int deterministic, int causal, int schedule) {
+  const int sch = resolve_sched(s, causal, schedule);
+  const int G = tile_for(s, causal, sch) == PairCfg::TILE ? 1 : head_group_for(s);
+  return ws_layout(s, resolved_split(s, deterministic, causal, schedule), G);
 }
 
 // Ticket-wait watchdog (clock64 cycles): default ~35 s at 1.965 GHz.
@@ -301,9 +328,12 @@ thread_local int g_trace_cap = 0;
 thread_local float* g_dump = nullptr;
 
 // Optional per-kernel event timing (dash_profile_begin/end).
+// Events are recorded at the start of a call (tag 0) and after each launch
+// (tag 1 = K1 preprocess, 2 = K2 main, 3 = K4 convert; a chunked call has one
+// 2, 3 pair per chunk); dash_profile_end sums each interval under its tag.
 struct ProfState {
   bool on = false;
-  std::vector<cudaEvent_t> ev;  // 4 per call
+  std::vector<std::pair<cudaEvent_t, int>> ev;
   std::vector<cudaEvent_t> pool;
   cudaEvent_t get() {
     if (!pool.empty()) {
@@ -320,12 +350,21 @@ ProfState& prof() {
   static ProfState p;
   return p;
 }
-void prof_mark(cudaStream_t st) {
+void prof_mark(cudaStream_t st, int tag) {
   ProfState& p = prof();
   if (!p.on) return;
   cudaEvent_t e = p.get();
   cudaEventRecord(e, st);
-  p.ev.push_back(e);
+  p.ev.emplace_back(e, tag);
+}
+
+// Between chunks: tickets and the job counter back to 0 (the error flag, the
+// word after the counter, keeps what earlier chunks set); the atomic variant
+// also re-zeroes its accumulator.
+cudaError_t reset_chunk(char* ws, const WsLayout& w, int deterministic, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(ws + w.tickets, 0, w.counters + 4 - w.tickets, st);
+  if (e == cudaSuccess && !deterministic) e = cudaMemsetAsync(ws + w.dqacc, 0, w.dqacc_bytes, st);
+  return e;
 }
 
 template <int D>
@@ -336,7 +375,8 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
   using C = BwdCfg<D>;
   const int n = s->seqlen / 128;
   const int W = resolved_split(s, deterministic, causal, schedule);  // once: K2 and K4 agree
-  const WsLayout w = ws_layout(s, W);
+  const int G = head_group_for(s);
+  const WsLayout w = ws_layout(s, W, G);
   // The setting may have changed since the workspace was sized.
   if (workspace_bytes < w.total) return DASH_ERR_WORKSPACE;
   const ScheduleTable* tab = cached_schedule(schedule, n, causal ? kCausal : kFull);
@@ -344,11 +384,11 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return DASH_ERR_CUDA;
   const int sms = device_sms(dev);
-  const int G = head_group_for(s);
-  const int total_jobs = tab->jobs * (s->batch * s->heads / G);
-  int grid = total_jobs < sms ? total_jobs : sms;
+  const int max_jobs = tab->jobs * (w.chunk / G);  // per launch (one chunk of heads)
+  const int grid = max_jobs < sms ? max_jobs : sms;
 
-  if (schedule == kShift && tab->coresident > grid) return DASH_ERR_UNSUPPORTED;
+  if (schedule == kShift && tab->coresident > (tab->jobs < sms ? tab->jobs : sms))
+    return DASH_ERR_UNSUPPORTED;
   const DevTable* dt = device_table(dev, tab, G);
   if (!dt) return DASH_ERR_CUDA;
 
@@ -368,8 +408,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
             make_map_2d(&tdo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, HD, BN, 64, C::BR);
   if (ok && !C::LINEAR)  // d = 64 reduces through a 2-D map of the W planes
     ok = make_map_2d(&tacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dqacc, D,
-                     static_cast<uint64_t>(W) * BN * static_cast<uint64_t>(s->heads), 32,
-                     C::STG_ROWS);
+                     static_cast<uint64_t>(W) * w.chunk * s->seqlen, 32, C::STG_ROWS);
   else
     tacc = tq;  // unused at d = 128 (1-D bulk reduces)
   if (!ok) {  // tensor map encoding (reported as -1 by dash_last_cuda_error)
@@ -382,7 +421,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
 
   const int poison = g_poison;
   g_poison = 0;
-  prof_mark(stream);
+  prof_mark(stream, 0);
   // K1: D, ticket / counter / error-flag reset, dQacc zero-fill for the atomic variant.
   {
     const size_t rows = BN * s->heads;
@@ -395,8 +434,9 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
         deterministic ? nullptr : reinterpret_cast<float4*>(dqacc),
         deterministic ? 0 : w.dqacc_bytes / 16, counters, poison);
   }
-  prof_mark(stream);
-  // K2: the persistent ordered-reduction backward.
+  prof_mark(stream, 1);
+  // Per chunk of heads (one chunk unless the planes exceed the budget):
+  // K2, the persistent ordered-reduction backward, then K4.
   {
     BwdArgs a;
     a.lse2 = lse2;
@@ -412,7 +452,6 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     a.N = s->seqlen;
     a.H = s->heads;
     a.jobs_per_head = tab->jobs;
-    a.total_jobs = total_jobs;
     a.scale = eff_scale(s);
     a.scale_log2 = a.scale * 1.4426950408889634f;
     a.causal = causal ? 1 : 0;
@@ -441,34 +480,39 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
         (!no_prefetch && (!deterministic || (schedule == kDescending && a.split >= 4))) ? 1 : 0;
     a.cyclic = (deterministic && schedule == kShift) ? 1 : 0;
     a.head_group = G;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(C::NTHREADS);
-    cfg.dynamicSmemBytes = C::SMEM_BYTES;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for SHIFT (AMB-12)
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tdo, tacc, a);
-    if (le != cudaSuccess) {
-      g_last_cuda = 10000 + static_cast<int>(le);  // launch of the main kernel
-      return DASH_ERR_CUDA;
+    const int BH = s->batch * s->heads;
+    for (int c = 0; c < w.chunks; ++c) {
+      a.bh_base = c * w.chunk;
+      a.bh_count = std::min(w.chunk, BH - a.bh_base);
+      a.total_jobs = tab->jobs * (a.bh_count / G);
+      if (c > 0 && reset_chunk(ws, w, deterministic, stream) != cudaSuccess) return cuda_check_last();
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(std::min(grid, a.total_jobs));
+      cfg.blockDim = dim3(C::NTHREADS);
+      cfg.dynamicSmemBytes = C::SMEM_BYTES;
+      cfg.stream = stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for SHIFT (AMB-12)
+      attr[0].val.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tdo, tacc, a);
+      if (le != cudaSuccess) {
+        g_last_cuda = 10000 + static_cast<int>(le);  // launch of the main kernel
+        return DASH_ERR_CUDA;
+      }
+      prof_mark(stream, 2);
+      // K4: dQ = bf16(scale * (acc_0 + ... + acc_{W-1})) for the chunk's heads.
+      const size_t total = static_cast<size_t>(a.bh_count) * s->seqlen * (D / 8);
+      const int block = 256;
+      size_t g = (total + block - 1) / block;
+      if (g > static_cast<size_t>(sms) * 16) g = static_cast<size_t>(sms) * 16;
+      dash_dq_convert_kernel<D><<<static_cast<unsigned>(g), block, 0, stream>>>(
+          dqacc, static_cast<__nv_bfloat16*>(dq), s->seqlen, s->heads, eff_scale(s), W,
+          causal ? 1 : 0, 128, a.bh_base, a.bh_count);
+      prof_mark(stream, 3);
     }
   }
-  prof_mark(stream);
-  // K4: dQ = bf16(scale * (acc_0 + ... + acc_{W-1})).
-  {
-    const size_t total = BN * s->heads * (D / 8);
-    const int block = 256;
-    size_t g = (total + block - 1) / block;
-    if (g > static_cast<size_t>(sms) * 16) g = static_cast<size_t>(sms) * 16;
-    dash_dq_convert_kernel<D><<<static_cast<unsigned>(g), block, 0, stream>>>(
-        dqacc, static_cast<__nv_bfloat16*>(dq), s->batch, s->seqlen, s->heads, eff_scale(s), W,
-        causal ? 1 : 0, 128);
-  }
-  prof_mark(stream);
   return cuda_check_last();
 }
 
@@ -504,6 +548,7 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
   const int W = resolved_split(s, deterministic, causal, schedule);
   const WsLayout w = ws_layout(s, W);
   if (workspace_bytes < w.total) return DASH_ERR_WORKSPACE;
+  const int BH = s->batch * s->heads;
   const ScheduleTable* tab = cached_schedule(schedule, n, causal ? kCausal : kFull);
   if (!tab) return DASH_ERR_UNSUPPORTED;
   int dev = 0;
@@ -513,9 +558,10 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
     return cuda_check_last();
   const int sms = device_sms(dev);
   const int max_cl = max_pair_clusters<NQS, NQK, NDS>(dev);
-  const int total_jobs = tab->jobs * (s->batch * s->heads);
-  const int clusters = total_jobs < max_cl ? total_jobs : max_cl;
-  if (schedule == kShift && tab->coresident > clusters) return DASH_ERR_UNSUPPORTED;
+  const int max_jobs = tab->jobs * w.chunk;  // per launch (one chunk of heads)
+  const int clusters = max_jobs < max_cl ? max_jobs : max_cl;
+  if (schedule == kShift && tab->coresident > (tab->jobs < max_cl ? tab->jobs : max_cl))
+    return DASH_ERR_UNSUPPORTED;
   const DevTable* dt = device_table(dev, tab, 1);
   if (!dt) return DASH_ERR_CUDA;
 
@@ -537,14 +583,14 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
       make_map_2d(&tdo32, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, HD, BN, 64, 32) &&
       make_map_2d(&tdo64, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, HD, BN, 64, 64) &&
       make_map_2d(&tacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dqacc, D,
-                  static_cast<uint64_t>(W) * BN * static_cast<uint64_t>(s->heads), 32, C::BR);
+                  static_cast<uint64_t>(W) * w.chunk * s->seqlen, 32, C::BR);
   if (!ok) {
     g_last_cuda = -1;
     return DASH_ERR_CUDA;
   }
   const int poison = g_poison;
   g_poison = 0;
-  prof_mark(stream);
+  prof_mark(stream, 0);
   {
     const size_t rows = BN * s->heads;
     const size_t threads = rows * (D / 8);
@@ -556,7 +602,7 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
         deterministic ? nullptr : reinterpret_cast<float4*>(dqacc),
         deterministic ? 0 : w.dqacc_bytes / 16, counters, poison);
   }
-  prof_mark(stream);
+  prof_mark(stream, 1);
   {
     BwdArgs a;
     a.lse2 = lse2;
@@ -572,7 +618,6 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
     a.N = s->seqlen;
     a.H = s->heads;
     a.jobs_per_head = tab->jobs;
-    a.total_jobs = total_jobs;
     a.scale = eff_scale(s);
     a.scale_log2 = a.scale * 1.4426950408889634f;
     a.causal = causal ? 1 : 0;
@@ -592,29 +637,33 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
         (!no_prefetch && (!deterministic || (schedule == kDescending && a.split >= 4))) ? 1 : 0;
     a.cyclic = (deterministic && schedule == kShift) ? 1 : 0;
     a.head_group = 1;
-
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * clusters);
-    cfg.blockDim = dim3(C::NTHREADS);
-    cfg.dynamicSmemBytes = C::SMEM_BYTES;
-    cfg.stream = stream;
-    const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, tq32, tq64, tk, tv, tdo32, tdo64, tacc, a);
-    if (le != cudaSuccess) {
-      g_last_cuda = 10000 + static_cast<int>(le);
-      return DASH_ERR_CUDA;
+    for (int c = 0; c < w.chunks; ++c) {
+      a.bh_base = c * w.chunk;
+      a.bh_count = std::min(w.chunk, BH - a.bh_base);
+      a.total_jobs = tab->jobs * a.bh_count;
+      if (c > 0 && reset_chunk(ws, w, deterministic, stream) != cudaSuccess) return cuda_check_last();
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(2 * std::min(clusters, a.total_jobs));
+      cfg.blockDim = dim3(C::NTHREADS);
+      cfg.dynamicSmemBytes = C::SMEM_BYTES;
+      cfg.stream = stream;
+      const cudaError_t le =
+          cudaLaunchKernelEx(&cfg, kern, tq32, tq64, tk, tv, tdo32, tdo64, tacc, a);
+      if (le != cudaSuccess) {
+        g_last_cuda = 10000 + static_cast<int>(le);
+        return DASH_ERR_CUDA;
+      }
+      prof_mark(stream, 2);
+      const size_t total = static_cast<size_t>(a.bh_count) * s->seqlen * (D / 8);
+      const int block = 256;
+      size_t g = (total + block - 1) / block;
+      if (g > static_cast<size_t>(sms) * 16) g = static_cast<size_t>(sms) * 16;
+      dash_dq_convert_kernel<D><<<static_cast<unsigned>(g), block, 0, stream>>>(
+          dqacc, static_cast<__nv_bfloat16*>(dq), s->seqlen, s->heads, eff_scale(s), W,
+          causal ? 1 : 0, C::TILE, a.bh_base, a.bh_count);
+      prof_mark(stream, 3);
     }
   }
-  prof_mark(stream);
-  {
-    const size_t total = BN * s->heads * (D / 8);
-    const int block = 256;
-    size_t g = (total + block - 1) / block;
-    if (g > static_cast<size_t>(sms) * 16) g = static_cast<size_t>(sms) * 16;
-    dash_dq_convert_kernel<D><<<static_cast<unsigned>(g), block, 0, stream>>>(
-        dqacc, static_cast<__nv_bfloat16*>(dq), s->batch, s->seqlen, s->heads, eff_scale(s), W,
-        causal ? 1 : 0, C::TILE);
-  }
-  prof_mark(stream);
   return cuda_check_last();
 }
 
@@ -641,7 +690,7 @@ DASH_API const char* dash_version(void) { return "dash-b200 0.1 (sm_100a)"; }
 
 DASH_API dash_status dash_profile_begin(void) {
   ProfState& p = prof();
-  for (cudaEvent_t e : p.ev) p.pool.push_back(e);
+  for (auto& e : p.ev) p.pool.push_back(e.first);
   p.ev.clear();
   p.on = true;
   return DASH_OK;
@@ -651,24 +700,26 @@ DASH_API dash_status dash_profile_end(double* ms_pre, double* ms_main, double* m
                                       int* n_calls) {
   ProfState& p = prof();
   p.on = false;
-  double a = 0, b = 0, c = 0;
-  const size_t n = p.ev.size() / 4;
-  for (size_t i = 0; i < n; ++i) {
-    float t0 = 0, t1 = 0, t2 = 0;
-    if (cudaEventSynchronize(p.ev[4 * i + 3]) != cudaSuccess) return DASH_ERR_CUDA;
-    cudaEventElapsedTime(&t0, p.ev[4 * i], p.ev[4 * i + 1]);
-    cudaEventElapsedTime(&t1, p.ev[4 * i + 1], p.ev[4 * i + 2]);
-    cudaEventElapsedTime(&t2, p.ev[4 * i + 2], p.ev[4 * i + 3]);
-    a += t0;
-    b += t1;
-    c += t2;
+  double sum[4] = {0, 0, 0, 0};
+  int n = 0;
+  if (!p.ev.empty() && cudaEventSynchronize(p.ev.back().first) != cudaSuccess) return DASH_ERR_CUDA;
+  for (size_t i = 0; i < p.ev.size(); ++i) {
+    const int tag = p.ev[i].second;
+    if (tag == 0) {
+      ++n;
+      continue;
+    }
+    float t = 0;
+    if (i > 0) cudaEventElapsedTime(&t, p.ev[i - 1].first, p.ev[i].first);
+    sum[tag] += t;
   }
-  for (cudaEvent_t e : p.ev) p.pool.push_back(e);
+  for (auto& e : p.ev) p.pool.push_back(e.first);
   p.ev.clear();
+  const double a = sum[1], b = sum[2], c = sum[3];
   if (ms_pre) *ms_pre = a;
   if (ms_main) *ms_main = b;
   if (ms_post) *ms_post = c;
-  if (n_calls) *n_calls = static_cast<int>(n);
+  if (n_calls) *n_calls = n;
   return DASH_OK;
 }
 
@@ -725,7 +776,7 @@ DASH_API size_t dash_attn_bwd_workspace_bytes(const dash_shape* s, int causal, i
                                               int deterministic) {
   if (!shape_ok(s)) return 0;
   if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_AUTO) return 0;
-  return ws_layout(s, resolved_split(s, deterministic, causal, schedule)).total;
+  return layout_for(s, deterministic, causal, schedule).total;
 }
 
 DASH_API dash_status dash_attn_bwd(const dash_shape* s, const void* q, const void* k, const void* v,
@@ -800,6 +851,17 @@ DASH_API size_t dash_attn_bwd_dump_bytes(const dash_shape* s, int causal, int sc
   if (tile == 0) return 0;
   return static_cast<size_t>(s->batch) * s->heads * (s->seqlen / tile) * s->seqlen *
          s->head_dim * 4;
+}
+
+DASH_API dash_status dash_attn_bwd_set_plane_budget(size_t bytes) {
+  g_plane_budget = bytes == 0 ? kDefaultPlaneBudget : bytes;
+  return DASH_OK;
+}
+
+DASH_API int dash_attn_bwd_head_chunk(const dash_shape* s, int causal, int schedule,
+                                      int deterministic) {
+  if (!shape_ok(s) || schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_AUTO) return 0;
+  return layout_for(s, deterministic, causal, schedule).chunk;
 }
 
 DASH_API dash_status dash_attn_bwd_set_tile(int tile) {
@@ -878,8 +940,7 @@ HostPlan host_plan(const dash_shape* s, int causal, int schedule, int determinis
   h.lse = off;
   off = align_up(off + h.lse_bytes, kAlign);
   h.inner = off;
-  h.slot = align_up(off + ws_layout(&cs, resolved_split(&cs, deterministic, causal, schedule)).total,
-                    kAlign);
+  h.slot = align_up(off + layout_for(&cs, deterministic, causal, schedule).total, kAlign);
   h.total = kHostSlots * h.slot;
   return h;
 }
@@ -1011,7 +1072,7 @@ DASH_API dash_status dash_check_workspace(const dash_shape* s, int causal, int s
                                           int deterministic, const void* workspace, void* stream) {
   if (!shape_ok(s) || !workspace) return DASH_ERR_INVALID_ARG;
   if (schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_AUTO) return DASH_ERR_INVALID_ARG;
-  const WsLayout w = ws_layout(s, resolved_split(s, deterministic, causal, schedule));
+  const WsLayout w = layout_for(s, deterministic, causal, schedule);
   int flag = 0;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   int* dflag = reinterpret_cast<int*>(static_cast<char*>(const_cast<void*>(workspace)) + w.counters) + 1;

@@ -97,6 +97,10 @@ def _load():
     lib.dash_attn_bwd_tile.argtypes = [SP, i, i]
     lib.dash_attn_bwd_set_tile.restype = st
     lib.dash_attn_bwd_set_tile.argtypes = [i]
+    lib.dash_attn_bwd_set_plane_budget.restype = st
+    lib.dash_attn_bwd_set_plane_budget.argtypes = [ctypes.c_size_t]
+    lib.dash_attn_bwd_head_chunk.restype = i
+    lib.dash_attn_bwd_head_chunk.argtypes = [SP, i, i, i]
     return lib
 
 
@@ -222,6 +226,19 @@ def acc_split(shape_bnhd=None, causal: bool = True, schedule="auto") -> int:
 def set_acc_split(w: int):
     """dash_attn_bwd_set_acc_split (host-global)."""
     _check(_lib.dash_attn_bwd_set_acc_split(int(w)), "dash_attn_bwd_set_acc_split")
+
+
+def set_plane_budget(nbytes: int):
+    """dash_attn_bwd_set_plane_budget (host-global; 0 = default 4 GiB)."""
+    _check(_lib.dash_attn_bwd_set_plane_budget(int(nbytes)), "dash_attn_bwd_set_plane_budget")
+
+
+def head_chunk(shape_bnhd, causal: bool = True, schedule="auto", deterministic=True) -> int:
+    """dash_attn_bwd_head_chunk: flattened heads per launch under the dQ-plane budget."""
+    B, N, H, d = shape_bnhd
+    shp = Shape(B, N, H, d, 0.0)
+    return int(_lib.dash_attn_bwd_head_chunk(ctypes.byref(shp), int(causal), _sched(schedule),
+                                             int(deterministic)))
 
 
 def attn_bwd_dump(q, k, v, o, dout, lse, causal: bool, schedule, deterministic=True, scale=None,

@@ -17,10 +17,12 @@ import argparse
 import json
 import os
 import sys
+import time
 
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import ClockSampler  # noqa: E402
 from paper_2601_21824_b200.autograd import attention  # noqa: E402
 
 HIDDEN, HEADS, D, FFN = 4096, 32, 128, 14336
@@ -86,6 +88,9 @@ def main():
         cases = (("naive", "naive", True), ("descending", "descending", True),
                  ("shift", "shift", True), ("auto", "auto", True), ("atomic", "naive", False))
         times = {c[0]: [] for c in cases}
+        clk = ClockSampler(torch.cuda.current_device()).__enter__()  # clocks over the row's timings
+        time.sleep(0.3)
+        clk.mark("t0")
         for _ in range(3):  # round-robin over the cases, median per case
             for name, sched, det in cases:
                 def step():
@@ -106,6 +111,9 @@ def main():
             q.grad = k.grad = v.grad = None
             attention(q, k, v, True, "auto", True).backward(do)
         row["attention_auto_ms"] = time_step(attn_step)
+        clk.mark("t1")
+        clk.__exit__(None, None, None)
+        row["clocks"] = clk.summary()
         row["attention_share"] = row["attention_auto_ms"] / row["auto_ms"]
         row["speedup_auto_vs_naive"] = row["naive_ms"] / row["auto_ms"]
         row["speedup_atomic_vs_naive"] = row["naive_ms"] / row["atomic_ms"]

@@ -22,6 +22,7 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+from bench import ClockSampler  # noqa: E402
 from paper_2601_21824_b200 import dash  # noqa: E402
 from paper_2601_21824_b200.inputs import attn_inputs  # noqa: E402
 
@@ -86,19 +87,23 @@ def main():
             row = {"n": n, "N": N, "B": B, "H": H, "mask": "causal" if causal else "full",
                    "acc_split": dash.acc_split((B, N, H, d), causal),
                    "c_cycles": c, "r_cycles": r, "n_sm": sms, "heads_m": m}
-            t_naive = time_bwd(g, causal, "naive")
-            cp_naive = dash.schedule_critical_path(dash.NAIVE, n, n, mask, m, sms, c, r)
-            for name, sched in (("naive", dash.NAIVE), ("descending", dash.DESCENDING),
-                                ("shift", dash.SHIFT)):
-                try:
-                    cp = dash.schedule_critical_path(sched, n, n, mask, m, sms, c, r)
-                except dash.DashError as e:
-                    row[name] = {"error": str(e)}
-                    continue
-                t = t_naive if name == "naive" else time_bwd(g, causal, name)
-                row[name] = {"gpu_ms": t, "model_cycles": cp,
-                             "gpu_ratio_vs_naive": t / t_naive,
-                             "model_ratio_vs_naive": cp / cp_naive}
+            with ClockSampler(torch.cuda.current_device()) as clk:  # clocks over the row's timings
+                clk.mark("t0")
+                t_naive = time_bwd(g, causal, "naive")
+                cp_naive = dash.schedule_critical_path(dash.NAIVE, n, n, mask, m, sms, c, r)
+                for name, sched in (("naive", dash.NAIVE), ("descending", dash.DESCENDING),
+                                    ("shift", dash.SHIFT)):
+                    try:
+                        cp = dash.schedule_critical_path(sched, n, n, mask, m, sms, c, r)
+                    except dash.DashError as e:
+                        row[name] = {"error": str(e)}
+                        continue
+                    t = t_naive if name == "naive" else time_bwd(g, causal, name)
+                    row[name] = {"gpu_ms": t, "model_cycles": cp,
+                                 "gpu_ratio_vs_naive": t / t_naive,
+                                 "model_ratio_vs_naive": cp / cp_naive}
+                clk.mark("t1")
+            row["clocks"] = clk.summary()
             rows.append(row)
             print(json.dumps(row), flush=True)
     if args.out:

@@ -118,6 +118,38 @@ def test_workspace_bytes_and_shape_checks(dash):
     assert dash.host_workspace_bytes((1, 256, 1, 64), False) > dash.workspace_bytes((1, 256, 1, 64), False)
 
 
+def test_plane_budget_bounds_config4_workspace(dash):
+    """BASELINE config 4 (B = 8, H = 32, N = 32k, d = 128, causal): the W = 8
+    accumulators of all 256 heads would be 32 GiB; under the default 4 GiB
+    dQ-plane budget the heads run in chunks of 32 (8 launches) and the whole
+    workspace stays under 8 GiB.  Smaller budgets shrink the chunk; a budget
+    below one head's planes still runs one head per launch."""
+    cfg4 = (8, 32768, 32, 128)
+    per_head = 8 * 32768 * 128 * 4
+    try:
+        dash.set_plane_budget(0)
+        assert dash.acc_split(cfg4, True, "auto") == 8
+        assert dash.head_chunk(cfg4, True, "auto") == (4 << 30) // per_head == 32
+        ws = dash.workspace_bytes(cfg4, True, "auto")
+        assert ws < 8 << 30
+        assert ws >= 32 * per_head + 2 * 8 * 32 * 32768 * 4  # planes + D + lse2 of all heads
+        # the bench sweep shapes fit one chunk
+        for N in (512, 2048, 16384):
+            shp = (16384 // N, N, 16, 128)
+            assert dash.head_chunk(shp, True, "auto") == shp[0] * shp[2]
+        dash.set_plane_budget(3 * per_head + 5)
+        assert dash.head_chunk(cfg4, True, "auto") == 3
+        assert dash.workspace_bytes(cfg4, True, "auto") < ws
+        dash.set_plane_budget(1)
+        assert dash.head_chunk(cfg4, True, "auto") == 1
+        # the atomic variant has one accumulator: 8 x the heads per chunk
+        dash.set_plane_budget(0)
+        assert dash.head_chunk(cfg4, True, "auto", deterministic=False) == 256
+        assert dash.head_chunk((1, 200, 1, 64), True) == 0
+    finally:
+        dash.set_plane_budget(0)
+
+
 def test_bwd_rejects_bad_arguments_without_gpu(dash):
     """Argument validation happens before any device call."""
     lib = dash.lib()
