@@ -372,16 +372,14 @@ __global__ void __launch_bounds__(512, 1)
             job_slot[it_job & 1] = atomicAdd(args.job_counter, 1);
             mode = 1;
           } else if (args.prefetch) {
-            int peek = ptx::ld_relaxed(args.job_counter);
-            while (peek >= args.total_jobs ||
-                   peek / args.jobs_per_head != g / args.jobs_per_head) {
-              const int prev = atomicCAS(args.job_counter, peek, peek + 1);
-              if (prev == peek) {
-                job_slot[it_job & 1] = peek;
-                mode = 1;
-                break;
-              }
-              peek = prev;
+            // cyclic schedule: claim early only outside the current head.  The
+            // counter only grows, so once a (possibly stale) read of it lies
+            // beyond this head, every later claim does too -- one atomicAdd,
+            // no compare-and-swap loop (which serialises all CTAs' claims).
+            const int peek = ptx::ld_relaxed(args.job_counter);
+            if (peek / args.jobs_per_head != g / args.jobs_per_head) {
+              job_slot[it_job & 1] = atomicAdd(args.job_counter, 1);
+              mode = 1;
             }
           }
           // decision for job number it_job (the CTA's next job), slot (it_job - 1) % 2

@@ -147,7 +147,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
                          const __grid_constant__ CUtensorMap tm_v,
                          const __grid_constant__ CUtensorMap tm_do32,
                          const __grid_constant__ CUtensorMap tm_do64,
-                         const __grid_constant__ CUtensorMap tm_dqacc, const BwdArgs args) {
+                         const __grid_constant__ CUtensorMap tm_dqacc,
+                         const __grid_constant__ CUtensorMap tm_dk,
+                         const __grid_constant__ CUtensorMap tm_dv, const BwdArgs args) {
   using C = PairCfgT<NQS_, NQK_, NDS_>;
   constexpr int D = C::D, BR = C::BR, NSUB = C::NSUB, NQS = C::NQS, NQK = C::NQK;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -192,6 +194,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
     ptx::prefetch_tmap(&tm_do32);
     ptx::prefetch_tmap(&tm_do64);
     ptx::prefetch_tmap(&tm_dqacc);
+    ptx::prefetch_tmap(&tm_dk);
+    ptx::prefetch_tmap(&tm_dv);
   }
   if (warp == 1) ptx::tmem_alloc2<512>(tmem_slot);
   ptx::tc_fence_before();
@@ -267,6 +271,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
         const TaskView tv0 = decode_task(args, jv, args.tasks[ts]);
         // K / V / KB of this KV segment
         if (kv_cnt > 0) ptx::mbar_wait_u(&bars[P_KV_EMPTY], (kv_cnt - 1) & 1);
+        if (lane == 0) DASH_TRACE_MARK(20, q_cnt);
         if (ptx::aborted()) break;
         if (leader && lane == 0)
           ptx::mbar_arrive_expect_tx_local(&bars[P_KV_FULL], 2 * (2 * C::KV_BYTES + C::KB_BYTES));
@@ -306,8 +311,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
       if (leader) {
         if (args.prefetch) ptx::mbar_wait_u(&bars[P_KV_EMPTY], (kv_cnt - 1) & 1);
         if (lane == 0) {
+          DASH_TRACE_MARK(28, q_cnt);
           int mode = 2;
           if (it_job >= 2) ptx::mbar_wait_cluster(&bars[P_SLOT_FREE0 + (it_job & 1)], ((it_job - 2) >> 1) & 1);
+          DASH_TRACE_MARK(29, q_cnt);
           int next = -1;
           if (ptx::aborted()) {
             next = args.total_jobs;
@@ -316,18 +323,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
             next = atomicAdd(args.job_counter, 1);
             mode = 1;
           } else if (args.prefetch) {
-            int peek = ptx::ld_relaxed(args.job_counter);
-            while (peek >= args.total_jobs ||
-                   peek / args.jobs_per_head != g / args.jobs_per_head) {
-              const int prev = atomicCAS(args.job_counter, peek, peek + 1);
-              if (prev == peek) {
-                next = peek;
-                mode = 1;
-                break;
-              }
-              peek = prev;
+            // cyclic schedule: early claim only outside the current head (one
+            // atomicAdd once the counter is seen beyond it; see bwd.cuh)
+            const int peek = ptx::ld_relaxed(args.job_counter);
+            if (peek / args.jobs_per_head != g / args.jobs_per_head) {
+              next = atomicAdd(args.job_counter, 1);
+              mode = 1;
             }
           }
+          DASH_TRACE_MARK(30, q_cnt);
           claim_mode[(it_job - 1) & 1] = mode;
           ptx::mbar_arrive(&bars[P_PF0 + ((it_job - 1) & 1)]);
           if (mode == 1) {
@@ -428,6 +432,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
         ++kv_cnt;
         ptx::tc_fence_after();
         const uint32_t base = x;
+        if (lane == 0) DASH_TRACE_MARK(22, base);
         issue_sdp(base);
         for (uint32_t u = 0; u < nsub; ++u) {
           const uint32_t xx = base + u;
@@ -543,6 +548,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
             DASH_TRACE_MARK(12, x);
             if (det) {
               ptx::fence_async_global();
+              DASH_TRACE_MARK(17, x);
               ptx::st_release(ticket, rank_w + 1);
             }
             DASH_TRACE_MARK(9, x);
@@ -556,6 +562,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
             const uint32_t j1 = it_job + 1;
             if (j1 >= 2) ptx::mbar_wait_cluster(&bars[P_SLOT_FREE0 + (j1 & 1)], ((j1 - 2) >> 1) & 1);
             const int next = ptx::aborted() ? args.total_jobs : atomicAdd(args.job_counter, 1);
+            DASH_TRACE_MARK(21, x);
             job_slot[j1 & 1] = next;
             ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(&job_slot[j1 & 1]), 1),
                                 static_cast<uint32_t>(next));
@@ -691,10 +698,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
           ptx::mbar_wait(&bars[P_ACC_FULL], acc_cnt & 1);
           ++acc_cnt;
           ptx::tc_fence_after();
-          const size_t grow =
-              (static_cast<size_t>(tv.b) * args.N + kv * C::TILE + krow) * args.H + tv.h;
-          __nv_bfloat16* dvp = args.dv + grow * D;
-          __nv_bfloat16* dkp = args.dk + grow * D;
+          if (row == 0 && wg == 0) DASH_TRACE_MARK(18, x - 1);
+          // dK, dV rows of this warp (32 KV rows x this warpgroup's 64 d columns)
+          // go out through TMA stores of 32 x 32 bf16 boxes staged in the warp's
+          // 2 KB of the outbox: free here -- ACC_FULL follows the last dQ MMA,
+          // which waited for every dS^T copy out of it.  (Generic stores of one
+          // 16 B piece per row per lane are LSU-bound -- one L2 request per
+          // lane -- and keep the SM's store queue full under the reducers'
+          // release fences.)
+          uint8_t* ep = smem + C::OFF_OUT + (warp - 4) * 2048;
+          const int grow0 = tv.b * args.N + kv * C::TILE + C::BC * static_cast<int>(cta) + (warp & 3) * 32;
+          int nst = 0;
 #pragma unroll 1
           for (int c0 = wg * (D / C::NSMX); c0 < (wg + 1) * (D / C::NSMX); c0 += 32) {
             float a[32], k2[32];
@@ -702,27 +716,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
             ptx::tmem_ld32(tbase + lane_off + C::T_DK + c0, k2);
             ptx::tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; e += 8) {
-              uint4 pv, pk4;
-              pv.x = pack_bf16(a[e], a[e + 1]);
-              pv.y = pack_bf16(a[e + 2], a[e + 3]);
-              pv.z = pack_bf16(a[e + 4], a[e + 5]);
-              pv.w = pack_bf16(a[e + 6], a[e + 7]);
-              pk4.x = pack_bf16(k2[e] * args.scale, k2[e + 1] * args.scale);
-              pk4.y = pack_bf16(k2[e + 2] * args.scale, k2[e + 3] * args.scale);
-              pk4.z = pack_bf16(k2[e + 4] * args.scale, k2[e + 5] * args.scale);
-              pk4.w = pack_bf16(k2[e + 6] * args.scale, k2[e + 7] * args.scale);
-              *reinterpret_cast<uint4*>(dvp + c0 + e) = pv;
-              *reinterpret_cast<uint4*>(dkp + c0 + e) = pk4;
+            for (int which = 0; which < 2; ++which) {  // dV, then dK (x scale, AMB-1)
+              const float* src = which == 0 ? a : k2;
+              const float sc = which == 0 ? 1.f : args.scale;
+              if (nst > 0) {  // the previous box has been read out of the staging
+                if (lane == 0) ptx::bulk_wait_read<0>();
+                __syncwarp();
+              }
+#pragma unroll
+              for (int e = 0; e < 32; e += 8) {
+                uint4 pv;
+                pv.x = pack_bf16(src[e] * sc, src[e + 1] * sc);
+                pv.y = pack_bf16(src[e + 2] * sc, src[e + 3] * sc);
+                pv.z = pack_bf16(src[e + 4] * sc, src[e + 5] * sc);
+                pv.w = pack_bf16(src[e + 6] * sc, src[e + 7] * sc);
+                *reinterpret_cast<uint4*>(ep + lane * 64 + e * 2) = pv;
+              }
+              ptx::fence_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(which == 0 ? &tm_dv : &tm_dk, ep, tv.h * D + c0, grow0);
+                ptx::bulk_commit();
+              }
+              ++nst;
             }
           }
           ptx::tc_fence_before();
+          if (lane == 0) ptx::bulk_wait_read<0>();
           __syncwarp();
+          if (row == 0 && wg == 0) DASH_TRACE_MARK(19, x - 1);
           if (lane == 0) ptx::mbar_arrive_remote(lbar(P_ACC_EMPTY));
+          // every warp's staging has been read before any warp writes the
+          // outbox again (the next sub-tile's dS^T halves)
+          ptx::named_bar_sync(1, 256);
         }
         tk_cur = tk_nxt;
       }
     }
+    if (lane == 0) ptx::bulk_wait_all();  // dK / dV stores complete before the CTA retires
+    __syncwarp();
   } else {
     // ================== dQ drain (both CTAs): TMEM -> fp32 SW128 staging ==================
     // dQ^T of this CTA (M = 64 d rows per SM, N = 64 Q cols): lane l < 64 holds

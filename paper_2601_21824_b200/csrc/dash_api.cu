@@ -107,6 +107,28 @@ int head_group_for(const dash_shape* s) {
   return 1;
 }
 
+// Early claim of the next job (AMB-28(a); the producer claims once the
+// current job's MMAs have completed, before its last ordered adds are
+// released; for SHIFT only a job of another head).  Measured per schedule and
+// kernel (profiles/r02_experiments_early_claim.txt, both head dims, both
+// masks): it pays for SHIFT everywhere (-3 to -13 %), for DESCENDING on the
+// pair kernel and with the full mask, for NAIVE with the full mask, and for
+// the atomic variant; it costs up to 2-3x for causal NAIVE (the staircase: a
+// claimed job queued behind its CTA's reduction tail stalls the next head's
+// chain) unless a head has at most 2 jobs (-18 % there), and for causal
+// DESCENDING on the single-CTA kernel below W = 4.
+// DASH_EARLY_CLAIM = 0 / 1 forces it off / on (experiments; bit-exact either way).
+int early_claim(int schedule, int causal, int deterministic, int W, bool pair, int jobs_per_head) {
+  static const int forced = [] {
+    const char* e = std::getenv("DASH_EARLY_CLAIM");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (forced == 0 || forced == 1) return forced;
+  if (!deterministic || schedule == kShift) return 1;
+  if (schedule == kDescending) return (pair || !causal || W >= 4) ? 1 : 0;
+  return (!causal || jobs_per_head <= 2) ? 1 : 0;  // NAIVE
+}
+
 bool shape_ok(const dash_shape* s) {
   if (!s) return false;
   if (s->batch < 1 || s->heads < 1 || s->seqlen < 128 || s->seqlen % 128) return false;
@@ -259,7 +281,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 bool make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base,
-                 uint64_t inner, uint64_t outer, uint32_t box_inner, uint32_t box_outer) {
+                 uint64_t inner, uint64_t outer, uint32_t box_inner, uint32_t box_outer,
+                 CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {inner, outer};
@@ -267,7 +290,7 @@ bool make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* 
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
   return enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -463,21 +486,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     a.dqacc = dqacc;
     a.n_tickets = static_cast<int>(w.n_tickets);
     a.dump = g_dump;
-    static const int no_prefetch = [] {
-      const char* e = std::getenv("DASH_NO_PREFETCH");  // experiments only (bit-exact either way)
-      return e ? std::atoi(e) : 0;
-    }();
-    // Early claim of the next job (bwd.cuh, producer) -- measured per schedule
-    // (profiles/r01_experiments/prefetch_claim.txt): it pays for the atomic
-    // variant (no waits) and for DESCENDING with W >= 4 interleaved
-    // accumulators (automatic at n >= 64; its waits sit at each job's first Q
-    // tile); with W = 1 (config-5 model check) it is slower; it costs up to 2x
-    // where a claimed job, queued behind its CTA's reduction tail, stalls a
-    // chain of later jobs -- SHIFT (a head's cyclic jobs must run together),
-    // NAIVE causal (staircase) and DESCENDING with W = 2 at d = 64.  NAIVE keeps
-    // the claim-after-release of the FA3-style baseline.
-    a.prefetch =
-        (!no_prefetch && (!deterministic || (schedule == kDescending && a.split >= 4))) ? 1 : 0;
+    a.prefetch = early_claim(schedule, causal, deterministic, W, false, tab->jobs);
     a.cyclic = (deterministic && schedule == kShift) ? 1 : 0;
     a.head_group = G;
     const int BH = s->batch * s->heads;
@@ -574,7 +583,7 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
 
   const uint64_t HD = static_cast<uint64_t>(s->heads) * D;
   const uint64_t BN = static_cast<uint64_t>(s->batch) * s->seqlen;
-  CUtensorMap tq32, tq64, tk, tv, tdo32, tdo64, tacc;
+  CUtensorMap tq32, tq64, tk, tv, tdo32, tdo64, tacc, tdk, tdv;
   const bool ok =
       make_map_2d(&tq32, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, q, HD, BN, 64, 32) &&
       make_map_2d(&tq64, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, q, HD, BN, 64, 64) &&
@@ -583,7 +592,12 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
       make_map_2d(&tdo32, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, HD, BN, 64, 32) &&
       make_map_2d(&tdo64, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, HD, BN, 64, 64) &&
       make_map_2d(&tacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dqacc, D,
-                  static_cast<uint64_t>(W) * w.chunk * s->seqlen, 32, C::BR);
+                  static_cast<uint64_t>(W) * w.chunk * s->seqlen, 32, C::BR) &&
+      // dK / dV epilogue: 32 x 32 bf16 boxes (64 B rows, unswizzled staging)
+      make_map_2d(&tdk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dk, HD, BN, 32, 32,
+                  CU_TENSOR_MAP_SWIZZLE_NONE) &&
+      make_map_2d(&tdv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dv, HD, BN, 32, 32,
+                  CU_TENSOR_MAP_SWIZZLE_NONE);
   if (!ok) {
     g_last_cuda = -1;
     return DASH_ERR_CUDA;
@@ -629,12 +643,7 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
     a.dqacc = dqacc;
     a.n_tickets = static_cast<int>(w.n_tickets);
     a.dump = g_dump;
-    static const int no_prefetch = [] {
-      const char* e = std::getenv("DASH_NO_PREFETCH");
-      return e ? std::atoi(e) : 0;
-    }();
-    a.prefetch =
-        (!no_prefetch && (!deterministic || (schedule == kDescending && a.split >= 4))) ? 1 : 0;
+    a.prefetch = early_claim(schedule, causal, deterministic, W, true, tab->jobs);
     a.cyclic = (deterministic && schedule == kShift) ? 1 : 0;
     a.head_group = 1;
     for (int c = 0; c < w.chunks; ++c) {
@@ -648,7 +657,7 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
       cfg.dynamicSmemBytes = C::SMEM_BYTES;
       cfg.stream = stream;
       const cudaError_t le =
-          cudaLaunchKernelEx(&cfg, kern, tq32, tq64, tk, tv, tdo32, tdo64, tacc, a);
+          cudaLaunchKernelEx(&cfg, kern, tq32, tq64, tk, tv, tdo32, tdo64, tacc, tdk, tdv, a);
       if (le != cudaSuccess) {
         g_last_cuda = 10000 + static_cast<int>(le);
         return DASH_ERR_CUDA;

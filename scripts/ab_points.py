@@ -1,0 +1,43 @@
+"""A/B helper: main-kernel time per call (CUDA events, dash_profile) at every
+sweep point of the hd128 (or --d 64) sweep, for the given schedules and masks.
+Experiment switches come from the environment of the process.
+
+  python scripts/ab_points.py TAG [--d 128] [--scheds auto,shift] [--full]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2601_21824_b200 import dash  # noqa: E402
+from paper_2601_21824_b200.inputs import attn_inputs, sweep_shape  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("tag")
+ap.add_argument("--d", type=int, default=128)
+ap.add_argument("--scheds", default="auto")
+ap.add_argument("--masks", default="causal")
+ap.add_argument("--seqlens", default="512,1024,2048,4096,8192,16384")
+ap.add_argument("--reps", type=int, default=10)
+args = ap.parse_args()
+res = {"tag": args.tag}
+for mask in args.masks.split(","):
+    causal = mask == "causal"
+    for N in (int(s) for s in args.seqlens.split(",")):
+        B, N, H, d = sweep_shape(N, args.d)
+        g = {k: v.cuda() for k, v in attn_inputs(B, N, H, d, seed=N).items()}
+        o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], causal)
+        for sched in args.scheds.split(","):
+            ws = dash.alloc_workspace(g["q"].shape, causal, sched, True, "cuda")
+            for _ in range(3):
+                dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal, sched, True, workspace=ws)
+            torch.cuda.synchronize()
+            dash.profile_begin()
+            for _ in range(args.reps):
+                dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal, sched, True, workspace=ws)
+            pre, main, post, n = dash.profile_end()
+            res[f"{mask}/{sched}/{N}"] = round(1000 * main / n, 1)  # us per call
+print(json.dumps(res))
