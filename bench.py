@@ -483,8 +483,35 @@ def sweep_rows(dash, torch, probs, causal, steps):
         if row.get("naive_w1") is not None and row.get("best_dash") is not None:
             row["gap_closed_incl_amb27"], row["pass_incl_amb27"] = gap_gate(
                 row["naive_w1"], row["best_dash"], row["atomic"])
+        row["dag_model"] = dag_model_row(dash, torch, s, causal, row["tile"])
         rows.append(row)
     return rows
+
+
+DAG_C, DAG_R = 3, 1  # task compute : ordered hand-off, ~8.6 k : ~3 k cycles per 256-row task
+
+
+def dag_model_row(dash, torch, s, causal, tile):
+    """The paper's DAG model (§3; dash_schedule_critical_path) at this
+    sweep point on the units the kernel keeps co-resident (CTA pairs for
+    256-row tiles, CTAs for 128-row tiles): critical path of each schedule and
+    whether it predicts DESCENDING or SHIFT to beat NAIVE at all.  Where it
+    does not, the same-W gate cannot pass on this device for a reason the
+    paper's own model reproduces (partially co-resident heads)."""
+    B, N, H, _ = s
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    units = sms // 2 if tile == 256 else sms
+    n = N // tile
+    mask = dash.CAUSAL if causal else dash.FULL
+    cp = {}
+    for name, sched in (("naive", dash.NAIVE), ("descending", dash.DESCENDING), ("shift", dash.SHIFT)):
+        try:
+            cp[name] = dash.schedule_critical_path(sched, n, n, mask, B * H, units, DAG_C, DAG_R)
+        except dash.DashError:
+            cp[name] = None
+    best = min(v for k, v in cp.items() if k != "naive" and v is not None)
+    return {"units": units, "n": n, "heads": B * H, "c": DAG_C, "r": DAG_R, "critical_path": cp,
+            "best_over_naive": best / cp["naive"], "predicts_dash_faster": best < cp["naive"]}
 
 
 def gate_summary(rows):
@@ -493,6 +520,9 @@ def gate_summary(rows):
                                   for r in rows],
             "pass_w1": [r.get("pass_w1") for r in rows],
             "all_pass_same_w": all(bool(r.get("pass")) for r in rows),
+            "dag_model_predicts_dash_faster": [r["dag_model"]["predicts_dash_faster"] for r in rows],
+            "fail_explained_by_dag_model": [bool(not r.get("pass") and
+                                                 not r["dag_model"]["predicts_dash_faster"]) for r in rows],
             "seqlens": [r["seqlen"] for r in rows]}
 
 

@@ -274,15 +274,18 @@ dash_status dash_attn_bwd_inject_fault(int poison);
 /* Schedule tile size T (B_r = B_c, AMB-11 / AMB-31) a dash_attn_bwd with
  * these arguments runs with: 256 -- the CTA-pair kernel (a cluster of two
  * CTAs per 256-row KV tile, cta_group::2 MMAs, one dQ partial per 256 KV
- * rows) -- at d = 128 when N is a multiple of 256 (and, for SHIFT, the
- * head's jobs fit the device's CTA pairs), else 128 (the single-CTA kernel).
- * The schedules, ranks and the DAG model are those of the paper with n =
- * N / T tiles.  0 for an invalid shape or schedule. */
+ * rows) -- at d = 128 when N is a multiple of 256 and N >= 4096 (full mask:
+ * N >= 2048), else 128 (the single-CTA kernel, which measured faster on
+ * shorter heads: more, shorter jobs); for SHIFT only when the head's jobs fit
+ * the device's CTA pairs.  Depends on (N, d, mask, schedule) only, never on
+ * B or H.  The schedules, ranks and the DAG model are those of the paper with
+ * n = N / T tiles.  0 for an invalid shape or schedule. */
 int dash_attn_bwd_tile(const dash_shape* shape, int causal, int schedule);
 
-/* 0 = automatic (the rule above), 128 = always the single-CTA kernel.
- * Host-global; DASH_ERR_INVALID_ARG for other values.  DASH_TILE in the
- * environment sets the initial value. */
+/* 0 = automatic (the rule above), 128 = always the single-CTA kernel, 256 =
+ * the CTA-pair kernel wherever it applies (d = 128, N a multiple of 256, a
+ * SHIFT head fits the device's pairs).  Host-global; DASH_ERR_INVALID_ARG for
+ * other values.  DASH_TILE in the environment sets the initial value. */
 dash_status dash_attn_bwd_set_tile(int tile);
 
 /* dQ-plane budget.  The W fp32 dQ accumulators (AMB-27) of all B*H heads take

@@ -158,6 +158,7 @@ struct BwdCfg {
   static_assert(T_PT + BR / 2 + (DS_IN_TMEM ? BR / 2 : 0) == 512, "TMEM budget");
   static_assert(SMEM_BYTES <= 232448, "smem budget");
   static_assert(SMX_COLS % 32 == 0, "softmax column split");
+  static_assert(NDS * P_BYTES >= 8 * 4096, "dK/dV epilogue staging (4 KB per softmax warp)");
 };
 
 // Barrier slots (arrival count in parentheses)
@@ -245,7 +246,9 @@ template <int D>
 __global__ void __launch_bounds__(512, 1)
     dash_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
-                    const __grid_constant__ CUtensorMap tm_dqacc, const BwdArgs args) {
+                    const __grid_constant__ CUtensorMap tm_dqacc,
+                    const __grid_constant__ CUtensorMap tm_dk,
+                    const __grid_constant__ CUtensorMap tm_dv, const BwdArgs args) {
   using C = BwdCfg<D>;
   constexpr int BR = C::BR, NSUB = C::NSUB, NSTAGE = C::NSTAGE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -290,6 +293,8 @@ __global__ void __launch_bounds__(512, 1)
     ptx::prefetch_tmap(&tm_v);
     ptx::prefetch_tmap(&tm_do);
     if constexpr (!C::LINEAR) ptx::prefetch_tmap(&tm_dqacc);
+    ptx::prefetch_tmap(&tm_dk);
+    ptx::prefetch_tmap(&tm_dv);
   }
   if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
@@ -731,15 +736,24 @@ __global__ void __launch_bounds__(512, 1)
           ptx::mbar_wait(&bars[B_ACC_FULL], acc_cnt & 1);
           ++acc_cnt;
           ptx::tc_fence_after();
-          const size_t grow = (static_cast<size_t>(tv.b) * args.N + kv * 128 + row) * args.H + tv.h;
-          __nv_bfloat16* dvp = args.dv + grow * D;
-          __nv_bfloat16* dkp = args.dk + grow * D;
+          // dK, dV rows of this warp (32 KV rows x this warpgroup's columns) go
+          // out through TMA stores of 32 x 32 bf16 boxes staged in the warp's
+          // 4 KB of the dS^T buffers: free here -- ACC_FULL follows every MMA
+          // of the segment -- and rewritten only by these warps after the
+          // named barrier below (generic stores of one 16 B piece per row per
+          // lane are LSU-bound and slow the reducers' release fences).
+          uint8_t* ep = smem + C::OFF_DS + (warp - 4) * 4096;
+          const int grow0 = tv.b * args.N + kv * 128 + (warp & 3) * 32;
 #pragma unroll 1
           for (int c0 = wg * (D / C::NSMX); c0 < (wg + 1) * (D / C::NSMX); c0 += 32) {
             float a[32], k2[32];
             ptx::tmem_ld32(tbase + lane_off + C::T_DV + c0, a);
             ptx::tmem_ld32(tbase + lane_off + C::T_DK + c0, k2);
             ptx::tmem_wait_ld();
+            if (c0 != wg * (D / C::NSMX)) {  // the previous chunk's boxes have been read
+              if (lane == 0) ptx::bulk_wait_read<0>();
+              __syncwarp();
+            }
 #pragma unroll
             for (int e = 0; e < 32; e += 8) {
               uint4 pv, pk;
@@ -751,16 +765,29 @@ __global__ void __launch_bounds__(512, 1)
               pk.y = pack_bf16(k2[e + 2] * args.scale, k2[e + 3] * args.scale);
               pk.z = pack_bf16(k2[e + 4] * args.scale, k2[e + 5] * args.scale);
               pk.w = pack_bf16(k2[e + 6] * args.scale, k2[e + 7] * args.scale);
-              *reinterpret_cast<uint4*>(dvp + c0 + e) = pv;
-              *reinterpret_cast<uint4*>(dkp + c0 + e) = pk;
+              *reinterpret_cast<uint4*>(ep + lane * 64 + e * 2) = pv;
+              *reinterpret_cast<uint4*>(ep + 2048 + lane * 64 + e * 2) = pk;
+            }
+            ptx::fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tm_dv, ep, tv.h * D + c0, grow0);
+              tma_store_2d(&tm_dk, ep + 2048, tv.h * D + c0, grow0);
+              ptx::bulk_commit();
             }
           }
           ptx::tc_fence_before();
+          if (lane == 0) ptx::bulk_wait_read<0>();
+          __syncwarp();
           ptx::mbar_arrive(&bars[B_ACC_EMPTY]);
+          // every warp's staging has been read before any warp writes dS^T again
+          ptx::named_bar_sync(1, 128 * C::NSMX);
         }
         tk_cur = tk_nxt;
       }
     }
+    if (lane == 0) ptx::bulk_wait_all();  // dK / dV stores complete before the CTA retires
+    __syncwarp();
   } else {
     // ================== dQ drain: TMEM -> fp32 staging ==================
     const int tl = (warp & 3) * 32 + lane;  // TMEM lane

@@ -108,8 +108,8 @@ using PairCfg = PairCfgT<>;
 // one instance per CTA, arrived on by multicast commits or locally.
 enum : int {
   P_JOB0 = 0, P_JOB1 = 1,        // (B) job slot filled (1; written by the leader)
-  P_KV_FULL = 2,                 // (L) K/V/KB of both CTAs loaded (1 + tx)
-  P_KV_EMPTY = 3,                // (B) K/V/KB consumed (commit)
+  P_KV_FULL = 2,                 // (L) K / V of both CTAs loaded (1 + tx)
+  P_KV_EMPTY = 3,                // (B) every MMA of the KV segment complete: KB free (commit)
   P_S_FULL = 4,                  // (B) S^T / dP^T in TMEM (commit)
   P_S_EMPTY = 5,                 // (L) both softmaxes read S^T / dP^T (16 warps)
   P_P_FULL = 6,                  // (L) both wrote P^T / dS^T to TMEM, own dS^T half to smem (16)
@@ -136,7 +136,11 @@ enum : int {
                                  // softmax warps stored their rows (4) and the partner's 8 KB
                                  // landed (tx); in the leader also the peer's relay (+1): the
                                  // dQ issuer waits on it
-  P_COUNT = 47
+  P_KB_FULL = 47,                // (L) KB of both CTAs loaded (1 + tx)
+  P_KV_FREE = 48,                // (B) K / V read by the segment's last S^T / dP^T (commit):
+                                 // the next segment's K / V load starts while its last
+                                 // sub-tile's softmax, dK / dV and dQ still run
+  P_COUNT = 49
 };
 
 template <int NQS_, int NQK_, int NDS_>
@@ -269,29 +273,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
         int te = ts + 1;
         while (te < jv.t1 && task_seg(args.tasks[te]) == seg) ++te;
         const TaskView tv0 = decode_task(args, jv, args.tasks[ts]);
-        // K / V / KB of this KV segment
-        if (kv_cnt > 0) ptx::mbar_wait_u(&bars[P_KV_EMPTY], (kv_cnt - 1) & 1);
+        // K / V of this KV segment: free once the previous segment's last
+        // S^T / dP^T completed (KV_FREE) -- before its last softmax / dK / dV / dQ
+        if (kv_cnt > 0) ptx::mbar_wait_u(&bars[P_KV_FREE], (kv_cnt - 1) & 1);
         if (lane == 0) DASH_TRACE_MARK(20, q_cnt);
         if (ptx::aborted()) break;
         if (leader && lane == 0)
-          ptx::mbar_arrive_expect_tx_local(&bars[P_KV_FULL], 2 * (2 * C::KV_BYTES + C::KB_BYTES));
+          ptx::mbar_arrive_expect_tx_local(&bars[P_KV_FULL], 2 * (2 * C::KV_BYTES));
         __syncwarp();
-        {
-          const int r_own = tv0.b * args.N + tv0.kv * C::TILE + C::BC * cta;
-          const int r_t0 = tv0.b * args.N + tv0.kv * C::TILE;
+        const int r_own = tv0.b * args.N + tv0.kv * C::TILE + C::BC * cta;
+        const int r_t0 = tv0.b * args.N + tv0.kv * C::TILE;
 #pragma unroll
-          for (int blk = 0; blk < 2; ++blk) {
-            ptx::tma_load_2d_pair_e(smem + C::OFF_K + blk * C::BC * 128, &tm_k, kv_full,
-                                    tv0.h * D + blk * 64, r_own);
-            ptx::tma_load_2d_pair_e(smem + C::OFF_V + blk * C::BC * 128, &tm_v, kv_full,
-                                    tv0.h * D + blk * 64, r_own);
-            // KB rows [128 blk, +128) = block `cta` of the KV rows of CTA blk
-            ptx::tma_load_2d_pair_e(smem + C::OFF_KB + blk * C::BC * 128, &tm_k, kv_full,
-                                    tv0.h * D + static_cast<int>(cta) * 64, r_t0 + blk * C::BC);
-          }
+        for (int blk = 0; blk < 2; ++blk) {
+          ptx::tma_load_2d_pair_e(smem + C::OFF_K + blk * C::BC * 128, &tm_k, kv_full,
+                                  tv0.h * D + blk * 64, r_own);
+          ptx::tma_load_2d_pair_e(smem + C::OFF_V + blk * C::BC * 128, &tm_v, kv_full,
+                                  tv0.h * D + blk * 64, r_own);
         }
         ++kv_cnt;
         load_qs(tv0, 0);
+        // KB (A of dQ^T): free once every MMA of the previous segment completed
+        if (kv_cnt > 1) ptx::mbar_wait_u(&bars[P_KV_EMPTY], (kv_cnt - 2) & 1);
+        if (leader && lane == 0)
+          ptx::mbar_arrive_expect_tx_local(&bars[P_KB_FULL], 2 * C::KB_BYTES);
+        __syncwarp();
+#pragma unroll
+        for (int blk = 0; blk < 2; ++blk) {
+          // KB rows [128 blk, +128) = block `cta` of the KV rows of CTA blk
+          ptx::tma_load_2d_pair_e(smem + C::OFF_KB + blk * C::BC * 128, &tm_k, lbar(P_KB_FULL),
+                                  tv0.h * D + static_cast<int>(cta) * 64, r_t0 + blk * C::BC);
+        }
         for (int t = ts; t < te; ++t) {
           const TaskView tv = decode_task(args, jv, args.tasks[t]);
           for (int sub = 0; sub < NSUB; ++sub) {
@@ -368,7 +379,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
     constexpr uint32_t ID_S = ptx::idesc_bf16(256, BR, 0, 0);     // S^T, dP^T
     constexpr uint32_t ID_KV = ptx::idesc_bf16(256, D, 0, 1);     // dV, dK (TS, B MN-major)
     constexpr uint32_t ID_Q = ptx::idesc_bf16(128, BR, 1, 1);     // dQ^T (A, B MN-major)
-    auto issue_sdp = [&](uint32_t xx) {
+    auto issue_sdp = [&](uint32_t xx, bool seg_last) {
       const uint32_t st = xx % NQS;
       ptx::mbar_wait_u(&bars[P_QS_FULL0 + st], (xx / NQS) & 1);
       if (xx > 0) ptx::mbar_wait_u(&bars[P_S_EMPTY], (xx - 1) & 1);
@@ -384,11 +395,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
                          dDOS + st * ST_STEP + kstep<false>(kk, 32), ID_S, kk > 0);
       ptx::mma2_commit_mc_e(&bars[P_S_FULL]);
       ptx::mma2_commit_mc_e(&bars[P_QS_EMPTY0 + st]);
+      if (seg_last) ptx::mma2_commit_mc_e(&bars[P_KV_FREE]);  // K / V no longer read
     };
+    bool kb_ready = false;  // KB of the current segment seen loaded
     // dQ_local^T = K^T dS^T over the 256 KV rows of the pair (Alg.1 line 28):
     // both DS buffers complete (P_DSR), the TMEM buffer drained (P_DQ_EMPTY)
     auto issue_dq = [&](uint32_t xx) {
       const uint32_t sb = xx % C::NDS, qb = xx & 1;
+      if (!kb_ready) {
+        ptx::mbar_wait_u(&bars[P_KB_FULL], (kv_cnt - 1) & 1);
+        kb_ready = true;
+      }
       if (xx >= 2) ptx::mbar_wait_u(&bars[P_DQ_EMPTY0 + qb], ((xx >> 1) - 1) & 1);
       ptx::mbar_wait_u(&bars[P_DSR0 + sb], (xx / C::NDS) & 1);
       ptx::tc_fence_after();
@@ -433,13 +450,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
         ptx::tc_fence_after();
         const uint32_t base = x;
         if (lane == 0) DASH_TRACE_MARK(22, base);
-        issue_sdp(base);
+        kb_ready = false;
+        issue_sdp(base, nsub == 1);
         for (uint32_t u = 0; u < nsub; ++u) {
           const uint32_t xx = base + u;
           const uint32_t qk = xx % NQK;
           // S/dP of the next sub-tile go into the tensor pipe while the softmax
           // warps turn this one into P^T / dS^T (dQ is issued by the drain).
-          if (u + 1 < nsub) issue_sdp(xx + 1);
+          if (u + 1 < nsub) issue_sdp(xx + 1, u + 2 == nsub);
           // QK operands first (normally long loaded), so the reaction to
           // P_FULL is only the MMA issue
           ptx::mbar_wait_u(&bars[P_QK_FULL0 + qk], (xx / NQK) & 1);

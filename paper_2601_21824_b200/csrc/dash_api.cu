@@ -157,13 +157,17 @@ int pair_cluster_bound() {  // CTA pairs co-resident on the current device
     return 74;
   return n / 2;
 }
-// `schedule` already resolved (not AUTO).  SHIFT needs a head's jobs
+// `schedule` already resolved (not AUTO).  Automatic: the pair kernel from N =
+// 4096 (full mask: 2048) -- below, the single-CTA kernel measured faster
+// (profiles/r02_experiments_tile.txt: more, shorter jobs on 148 CTAs; e.g.
+// causal SHIFT 172 vs 193 us at N = 512).  SHIFT needs a head's jobs
 // co-resident (AMB-12): with 256-row tiles that is min(n', 128) CTA pairs for
 // the full mask, ceil(n'/2) for causal -- beyond the device's pairs the
 // single-CTA kernel (128-row tiles, up to 148 co-resident CTAs) runs instead.
 int tile_for(const dash_shape* s, int causal, int schedule) {
   const bool pair_ok = s->head_dim == 128 && s->seqlen % PairCfg::TILE == 0;
   if (g_tile == 128 || !pair_ok) return 128;
+  if (g_tile == 0 && s->seqlen < (causal ? 4096 : 2048)) return 128;
   if (schedule == kShift) {
     const ScheduleTable* t = cached_schedule(kShift, s->seqlen / PairCfg::TILE, causal ? kCausal : kFull);
     if (!t || t->coresident > pair_cluster_bound()) return 128;
@@ -424,11 +428,15 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
 
   const uint64_t HD = static_cast<uint64_t>(s->heads) * D;
   const uint64_t BN = static_cast<uint64_t>(s->batch) * s->seqlen;
-  CUtensorMap tq, tk, tv, tdo, tacc;
+  CUtensorMap tq, tk, tv, tdo, tacc, tdk, tdv;
   bool ok = make_map_2d(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, q, HD, BN, 64, C::BR) &&
             make_map_2d(&tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, k, HD, BN, 64, C::BC) &&
             make_map_2d(&tv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, v, HD, BN, 64, C::BC) &&
-            make_map_2d(&tdo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, HD, BN, 64, C::BR);
+            make_map_2d(&tdo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, HD, BN, 64, C::BR) &&
+            make_map_2d(&tdk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dk, HD, BN, 32, 32,
+                        CU_TENSOR_MAP_SWIZZLE_NONE) &&
+            make_map_2d(&tdv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dv, HD, BN, 32, 32,
+                        CU_TENSOR_MAP_SWIZZLE_NONE);
   if (ok && !C::LINEAR)  // d = 64 reduces through a 2-D map of the W planes
     ok = make_map_2d(&tacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dqacc, D,
                      static_cast<uint64_t>(W) * w.chunk * s->seqlen, 32, C::STG_ROWS);
@@ -505,7 +513,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
       attr[0].val.cooperative = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tdo, tacc, a);
+      const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tdo, tacc, tdk, tdv, a);
       if (le != cudaSuccess) {
         g_last_cuda = 10000 + static_cast<int>(le);  // launch of the main kernel
         return DASH_ERR_CUDA;

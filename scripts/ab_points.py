@@ -22,6 +22,8 @@ ap.add_argument("--scheds", default="auto")
 ap.add_argument("--masks", default="causal")
 ap.add_argument("--seqlens", default="512,1024,2048,4096,8192,16384")
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--tiles", default="0", help="dash_attn_bwd_set_tile values to compare (0 = library choice)")
+ap.add_argument("--rounds", type=int, default=1, help="interleaved rounds (median reported)")
 args = ap.parse_args()
 res = {"tag": args.tag}
 for mask in args.masks.split(","):
@@ -30,14 +32,25 @@ for mask in args.masks.split(","):
         B, N, H, d = sweep_shape(N, args.d)
         g = {k: v.cuda() for k, v in attn_inputs(B, N, H, d, seed=N).items()}
         o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], causal)
-        for sched in args.scheds.split(","):
-            ws = dash.alloc_workspace(g["q"].shape, causal, sched, True, "cuda")
-            for _ in range(3):
-                dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal, sched, True, workspace=ws)
-            torch.cuda.synchronize()
-            dash.profile_begin()
-            for _ in range(args.reps):
-                dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal, sched, True, workspace=ws)
-            pre, main, post, n = dash.profile_end()
-            res[f"{mask}/{sched}/{N}"] = round(1000 * main / n, 1)  # us per call
+        times = {}
+        for _ in range(args.rounds):
+            for tile in (int(t) for t in args.tiles.split(",")):
+                dash.set_tile(tile)
+                for sched in args.scheds.split(","):
+                    ws = dash.alloc_workspace(g["q"].shape, causal, sched, True, "cuda")
+                    for _ in range(3):
+                        dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal, sched, True,
+                                      workspace=ws)
+                    torch.cuda.synchronize()
+                    dash.profile_begin()
+                    for _ in range(args.reps):
+                        dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal, sched, True,
+                                      workspace=ws)
+                    pre, main, post, n = dash.profile_end()
+                    key = f"{mask}/{sched}/{N}" + (f"/t{tile}" if tile else "")
+                    times.setdefault(key, []).append(1000 * main / n)  # us per call
+                    del ws
+        dash.set_tile(0)
+        for key, v in times.items():
+            res[key] = round(sorted(v)[len(v) // 2], 1)
 print(json.dumps(res))

@@ -1,0 +1,6 @@
+#!/bin/bash
+# tile rule (single-CTA below 4096 causal / 2048 full) + single-CTA TMA epilogue: tests + bench
+cd "$GRAFT_REPO_ROOT"
+mkdir -p gpurun_out
+timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/ab_tests.txt 2>&1
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/ab_bench.json 2> gpurun_out/ab_bench.err

@@ -191,9 +191,19 @@ def test_auto_schedule_policy_and_acc_split(dash):
         # single-CTA kernel (d = 64, 128-row tiles): n = N / 128
         assert [dash.acc_split((1, N, 16, 64), True) for N in (512, 4096, 8192, 16384, 32768)] == \
             [2, 2, 4, 4, 8]
-        # CTA-pair kernel (d = 128, 256-row tiles): n = N / 256
+        # d = 128: single-CTA kernel (n = N / 128) below N = 4096 causal / 2048 full,
+        # then the CTA-pair kernel (n = N / 256)
+        assert [dash.tile((1, N, 16, 128), True) for N in (512, 2048, 4096, 32768)] == [128, 128, 256, 256]
+        assert [dash.tile((1, N, 16, 128), False) for N in (1024, 2048)] == [128, 256]
         assert [dash.acc_split((1, N, 16, 128), True) for N in (512, 2048, 4096, 8192, 16384, 32768)] == \
-            [1, 1, 2, 4, 4, 8]
+            [2, 2, 2, 4, 4, 8]
+        assert [dash.acc_split((1, N, 16, 128), False) for N in (1024, 2048, 4096)] == [2, 1, 2]
+        try:  # the pair kernel forced at short N: n' <= 8 -> the paper's single accumulator
+            dash.set_tile(256)
+            assert dash.tile((1, 512, 16, 128), True) == 256
+            assert [dash.acc_split((1, N, 16, 128), True) for N in (512, 2048)] == [1, 1]
+        finally:
+            dash.set_tile(0)
         assert dash.acc_split((1, 8192, 16, 128), True) == dash.acc_split((8, 8192, 32, 128), True)
         for w in (1, 2, 4, 8):
             dash.set_acc_split(w)

@@ -83,9 +83,31 @@ def test_forward_matches_oracle(dash, shape, causal):
 @pytest.mark.parametrize("det", [True, False])
 def test_backward_matches_oracle(dash, shape, causal, schedule, det):
     B, N, H, d = shape
-    n = N // 128
     _, g = _inputs(B, N, H, d, seed=0)
     _, _, dq, dk, dv = _run(dash, g, causal, schedule, det)
+    ref = _ref(B, N, H, d, causal, 0)
+    errs = {name: _nerr(x, ref[name]) for name, x in (("dq", dq), ("dk", dk), ("dv", dv))}
+    assert all(e <= GRAD_TOL for e in errs.values()), errs
+
+
+PAIR_SHAPES = [s for s in SHAPES if s[3] == 128 and s[1] % 256 == 0]
+
+
+@pytest.mark.parametrize("shape", PAIR_SHAPES)
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("schedule", ["naive", "descending", "shift"])
+@pytest.mark.parametrize("det", [True, False])
+def test_backward_matches_oracle_pair_kernel(dash, shape, causal, schedule, det):
+    """The same cases on the CTA-pair kernel (forced: the library picks the
+    single-CTA kernel at these short N)."""
+    B, N, H, d = shape
+    _, g = _inputs(B, N, H, d, seed=0)
+    dash.set_tile(256)
+    try:
+        assert dash.tile(shape, causal, schedule) == 256
+        _, _, dq, dk, dv = _run(dash, g, causal, schedule, det)
+    finally:
+        dash.set_tile(0)
     ref = _ref(B, N, H, d, causal, 0)
     errs = {name: _nerr(x, ref[name]) for name, x in (("dq", dq), ("dk", dk), ("dv", dv))}
     assert all(e <= GRAD_TOL for e in errs.values()), errs
@@ -105,10 +127,20 @@ def test_backward_peaky_softmax(dash, causal):
 
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("schedule", ["naive", "descending", "shift"])
-def test_bitwise_determinism_100_runs(dash, causal, schedule):
-    """Deterministic mode: 100 repeated runs give identical bits (Table 1)."""
+@pytest.mark.parametrize("tile", [0, 256])
+def test_bitwise_determinism_100_runs(dash, causal, schedule, tile):
+    """Deterministic mode: 100 repeated runs give identical bits (Table 1, P:213-218);
+    tile 0 = the library's choice (single-CTA kernel at N = 1024), 256 = the pair kernel."""
     B, N, H, d = 4, 1024, 8, 128
     _, g = _inputs(B, N, H, d, seed=1)
+    dash.set_tile(tile)
+    try:
+        _determinism_100(dash, g, causal, schedule)
+    finally:
+        dash.set_tile(0)
+
+
+def _determinism_100(dash, g, causal, schedule):
     o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], causal)
     ws = dash.alloc_workspace(g["q"].shape, causal, schedule, True)
     base = dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal, schedule, True, workspace=ws)

@@ -40,9 +40,9 @@ def _run(dash, g, causal, schedule, det, budget):
 
 
 @pytest.mark.parametrize("d,tile,N,causal,schedule", [
-    (128, 0, 2048, True, "descending"),   # CTA-pair kernel, W = 1
-    (128, 0, 4096, True, "descending"),   # pair, W = 2 (two planes per chunk)
-    (128, 0, 2048, False, "shift"),       # pair, full-mask cyclic schedule
+    (128, 256, 2048, True, "descending"),  # CTA-pair kernel, W = 1
+    (128, 0, 4096, True, "descending"),    # pair (library choice), W = 2 (two planes per chunk)
+    (128, 0, 2048, False, "shift"),        # pair, full-mask cyclic schedule
     (128, 128, 2048, True, "shift"),      # single-CTA kernel (128-row tiles), W = 2
     (64, 0, 2048, False, "naive"),        # d = 64 (2-D tensor-map reduce)
     (64, 0, 8192, True, "descending"),    # d = 64, W = 4, early claim

@@ -151,15 +151,16 @@ def test_partials_cover_exactly_the_visited_tiles(dash):
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("schedule", ["naive", "descending", "shift"])
 @pytest.mark.parametrize("W", [1, 2])
-def test_replay_single_cta_kernel_d128(dash, W, causal, schedule):
-    """d = 128 with N a multiple of 256 runs the CTA-pair kernel by default;
-    dash_attn_bwd_set_tile(128) forces the single-CTA kernel (128-row tiles),
-    whose ordered reduction is replayed here at the same shape."""
+@pytest.mark.parametrize("tile", [128, 256])
+def test_replay_both_kernels_d128(dash, tile, W, causal, schedule):
+    """d = 128, N = 512: the library runs the single-CTA kernel here
+    (dash_attn_bwd_tile); dash_attn_bwd_set_tile forces either kernel, and the
+    ordered reduction of each is replayed at the same shape."""
     old_w = dash.acc_split()
-    dash.set_tile(128)
+    dash.set_tile(tile)
     dash.set_acc_split(W)
     try:
-        assert dash.tile((1, 512, 2, 128), causal, schedule) == 128
+        assert dash.tile((1, 512, 2, 128), causal, schedule) == tile
         _replay(dash, W, 1, 512, 2, 128, causal, schedule)
     finally:
         dash.set_tile(0)

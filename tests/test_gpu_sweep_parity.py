@@ -52,12 +52,12 @@ def _nerr(x, ref):
 
 
 @pytest.mark.parametrize("N", [512, 1024])
-@pytest.mark.parametrize("d,tile", [(128, 0), (128, 128), (64, 0)],
+@pytest.mark.parametrize("d,tile", [(128, 256), (128, 128), (64, 0)],
                          ids=["d128-pair", "d128-single", "d64"])
 @pytest.mark.parametrize("causal", [True, False])
 def test_sweep_shape_every_schedule_full_tensor(dash, N, d, tile, causal):
-    """tile 0: the library's choice (the CTA-pair kernel with 256-row tiles at
-    d = 128); tile 128 forces the single-CTA kernel."""
+    """tile 256 forces the CTA-pair kernel (256-row tiles), tile 128 the
+    single-CTA kernel (the library's choice at these N)."""
     dash.set_tile(tile)
     try:
         _sweep_case(dash, N, d, causal)
