@@ -394,6 +394,38 @@ cudaError_t reset_chunk(char* ws, const WsLayout& w, int deterministic, cudaStre
   return e;
 }
 
+// K1 and K4 grids: one wave of 256-thread blocks (8 per SM), grid-stride.
+template <int D>
+void launch_preprocess(const dash_shape* s, const void* o, const void* dout, const float* lse,
+                       float* dvec, float* lse2, int* tickets, int n_tickets, float* zero,
+                       size_t n_zero_f4, int* counters, int poison, int sms, cudaStream_t stream) {
+  constexpr int RPB = 256 / (D / 8);
+  const size_t rows = static_cast<size_t>(s->batch) * s->seqlen * s->heads;
+  size_t g = (rows + 2 * RPB - 1) / (2 * RPB);
+  if (g > static_cast<size_t>(sms) * 8) g = static_cast<size_t>(sms) * 8;
+  dash_preprocess_kernel<D><<<static_cast<unsigned>(g), 256, 0, stream>>>(
+      static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse, dvec, lse2,
+      s->batch, s->seqlen, s->heads, tickets, n_tickets, reinterpret_cast<float4*>(zero), n_zero_f4,
+      counters, poison);
+}
+template <int D>
+void launch_convert(const dash_shape* s, const float* dqacc, void* dq, int W, int causal, int tile,
+                    int bh_base, int bh_count, int sms, cudaStream_t stream) {
+  const size_t total = static_cast<size_t>(bh_count) * s->seqlen * (D / 8);
+  size_t g = (total + 2 * 256 - 1) / (2 * 256);
+  if (g > static_cast<size_t>(sms) * 8) g = static_cast<size_t>(sms) * 8;
+  const dim3 grid(static_cast<unsigned>(g));
+  auto* out = static_cast<__nv_bfloat16*>(dq);
+  const float sc = eff_scale(s);
+  const int c = causal ? 1 : 0;
+  switch (W) {
+    case 1: dash_dq_convert_kernel<D, 1><<<grid, 256, 0, stream>>>(dqacc, out, s->seqlen, s->heads, sc, c, tile, bh_base, bh_count); break;
+    case 2: dash_dq_convert_kernel<D, 2><<<grid, 256, 0, stream>>>(dqacc, out, s->seqlen, s->heads, sc, c, tile, bh_base, bh_count); break;
+    case 4: dash_dq_convert_kernel<D, 4><<<grid, 256, 0, stream>>>(dqacc, out, s->seqlen, s->heads, sc, c, tile, bh_base, bh_count); break;
+    default: dash_dq_convert_kernel<D, 8><<<grid, 256, 0, stream>>>(dqacc, out, s->seqlen, s->heads, sc, c, tile, bh_base, bh_count); break;
+  }
+}
+
 template <int D>
 dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const void* v,
                        const void* o, const void* dout, const float* lse, void* dq, void* dk,
@@ -454,17 +486,9 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
   g_poison = 0;
   prof_mark(stream, 0);
   // K1: D, ticket / counter / error-flag reset, dQacc zero-fill for the atomic variant.
-  {
-    const size_t rows = BN * s->heads;
-    const size_t threads = rows * (D / 8);
-    const int block = 256;
-    const unsigned gridp = static_cast<unsigned>((threads + block - 1) / block);
-    dash_preprocess_kernel<D><<<gridp, block, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse, dvec,
-        lse2, s->batch, s->seqlen, s->heads, tickets, static_cast<int>(W * w.n_tickets),
-        deterministic ? nullptr : reinterpret_cast<float4*>(dqacc),
-        deterministic ? 0 : w.dqacc_bytes / 16, counters, poison);
-  }
+  launch_preprocess<D>(s, o, dout, lse, dvec, lse2, tickets, static_cast<int>(W * w.n_tickets),
+                       deterministic ? nullptr : dqacc, deterministic ? 0 : w.dqacc_bytes / 16,
+                       counters, poison, sms, stream);
   prof_mark(stream, 1);
   // Per chunk of heads (one chunk unless the planes exceed the budget):
   // K2, the persistent ordered-reduction backward, then K4.
@@ -520,13 +544,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
       }
       prof_mark(stream, 2);
       // K4: dQ = bf16(scale * (acc_0 + ... + acc_{W-1})) for the chunk's heads.
-      const size_t total = static_cast<size_t>(a.bh_count) * s->seqlen * (D / 8);
-      const int block = 256;
-      size_t g = (total + block - 1) / block;
-      if (g > static_cast<size_t>(sms) * 16) g = static_cast<size_t>(sms) * 16;
-      dash_dq_convert_kernel<D><<<static_cast<unsigned>(g), block, 0, stream>>>(
-          dqacc, static_cast<__nv_bfloat16*>(dq), s->seqlen, s->heads, eff_scale(s), W,
-          causal ? 1 : 0, 128, a.bh_base, a.bh_count);
+      launch_convert<D>(s, dqacc, dq, W, causal, 128, a.bh_base, a.bh_count, sms, stream);
       prof_mark(stream, 3);
     }
   }
@@ -613,17 +631,10 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
   const int poison = g_poison;
   g_poison = 0;
   prof_mark(stream, 0);
-  {
-    const size_t rows = BN * s->heads;
-    const size_t threads = rows * (D / 8);
-    const int block = 256;
-    const unsigned gridp = static_cast<unsigned>((threads + block - 1) / block);
-    dash_preprocess_kernel<D><<<gridp, block, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse, dvec,
-        lse2, s->batch, s->seqlen, s->heads, tickets, static_cast<int>(W * w.n_tickets),
-        deterministic ? nullptr : reinterpret_cast<float4*>(dqacc),
-        deterministic ? 0 : w.dqacc_bytes / 16, counters, poison);
-  }
+  // K1: D, ticket / counter / error-flag reset, dQacc zero-fill for the atomic variant.
+  launch_preprocess<D>(s, o, dout, lse, dvec, lse2, tickets, static_cast<int>(W * w.n_tickets),
+                       deterministic ? nullptr : dqacc, deterministic ? 0 : w.dqacc_bytes / 16,
+                       counters, poison, sms, stream);
   prof_mark(stream, 1);
   {
     BwdArgs a;
@@ -671,13 +682,7 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
         return DASH_ERR_CUDA;
       }
       prof_mark(stream, 2);
-      const size_t total = static_cast<size_t>(a.bh_count) * s->seqlen * (D / 8);
-      const int block = 256;
-      size_t g = (total + block - 1) / block;
-      if (g > static_cast<size_t>(sms) * 16) g = static_cast<size_t>(sms) * 16;
-      dash_dq_convert_kernel<D><<<static_cast<unsigned>(g), block, 0, stream>>>(
-          dqacc, static_cast<__nv_bfloat16*>(dq), s->seqlen, s->heads, eff_scale(s), W,
-          causal ? 1 : 0, C::TILE, a.bh_base, a.bh_count);
+      launch_convert<D>(s, dqacc, dq, W, causal, C::TILE, a.bh_base, a.bh_count, sms, stream);
       prof_mark(stream, 3);
     }
   }
