@@ -663,18 +663,30 @@ __global__ void __launch_bounds__(512, 1)
           if (row == 0 && wg == 0) DASH_TRACE_MARK(3, x);
           const float* Lrow = sL + st * BR;
           const float* Drow = sDv + st * BR;
-#pragma unroll 1
-          for (int ch = 0; ch < NC / 32; ++ch) {
-            const int cc0 = c_base + ch * 32;  // first Q row (column) of this chunk
-            float s[32], dp[32];
-            ptx::tmem_ld32(tbase + lane_off + C::T_S + cc0, s);
-            ptx::tmem_ld32(tbase + lane_off + C::T_DP + cc0, dp);
+          // NC columns in chunks of 16, software-pipelined: the TMEM loads of
+          // chunk ch + 1 are in flight while chunk ch is computed (wait::ld
+          // covers every outstanding load, so a chunk's load is issued right
+          // after the previous chunk's wait).  The S^T / dP^T columns are all
+          // read -- S_EMPTY -- before the last chunk is computed.
+          constexpr int CH = 16, NCH = NC / CH;
+          float s2[2][CH], dp2[2][CH];
+          ptx::tmem_ld16(tbase + lane_off + C::T_S + c_base, s2[0]);
+          ptx::tmem_ld16(tbase + lane_off + C::T_DP + c_base, dp2[0]);
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {
+            const int cur = ch & 1;
+            const int cc0 = c_base + ch * CH;  // first Q row (column) of this chunk
             ptx::tmem_wait_ld();
-            if (ch == NC / 32 - 1) {
+            if (ch + 1 < NCH) {
+              ptx::tmem_ld16(tbase + lane_off + C::T_S + cc0 + CH, s2[cur ^ 1]);
+              ptx::tmem_ld16(tbase + lane_off + C::T_DP + cc0 + CH, dp2[cur ^ 1]);
+            } else {
               ptx::tc_fence_before();
               ptx::mbar_arrive(&bars[B_S_EMPTY]);
             }
-            uint32_t pk[16], dk2[16];
+            const float* s = s2[cur];
+            const float* dp = dp2[cur];
+            uint32_t pk[CH / 2], dk2[CH / 2];
             // P = exp2(S*scale*log2e - L*log2e), dS = P o (dP - D), packed to bf16.
             // The causal mask (key row > query row) exists only on the diagonal
             // task; off the diagonal the per-element compare/select is skipped.
@@ -682,7 +694,7 @@ __global__ void __launch_bounds__(512, 1)
               constexpr bool MASKED = decltype(masked)::value;
               const int mask_from = row - sub * BR - cc0;  // masked: cols c < mask_from
 #pragma unroll
-              for (int c4 = 0; c4 < 8; ++c4) {
+              for (int c4 = 0; c4 < CH / 4; ++c4) {
                 const float4 l4 = *reinterpret_cast<const float4*>(Lrow + cc0 + c4 * 4);
                 const float4 d4 = *reinterpret_cast<const float4*>(Drow + cc0 + c4 * 4);
                 const float Lv[4] = {l4.x, l4.y, l4.z, l4.w};
@@ -708,17 +720,17 @@ __global__ void __launch_bounds__(512, 1)
             else smx(std::false_type{});
             // P^T -> TMEM once dV of sub-tile x - 1 consumed it.
             if (ch == 0 && x >= 1) ptx::mbar_wait(&bars[B_PT_EMPTY], (x - 1) & 1);
-            ptx::tmem_st16(tbase + lane_off + C::T_PT + cc0 / 2, pk);
+            ptx::tmem_st8(tbase + lane_off + C::T_PT + cc0 / 2, pk);
             if constexpr (C::DS_IN_TMEM) {
               // dS^T -> TMEM (A operand of the dK TS-MMA) once dK of x - 1 consumed it.
               if (ch == 0 && x >= 1) ptx::mbar_wait(&bars[B_DST_EMPTY], (x - 1) & 1);
-              ptx::tmem_st16(tbase + lane_off + C::T_DST + cc0 / 2, dk2);
+              ptx::tmem_st8(tbase + lane_off + C::T_DST + cc0 / 2, dk2);
             }
             // dS^T -> smem buffer sb once dK, dQ of sub-tile x - NDS consumed it.
             if (ch == 0 && x >= C::NDS)
               ptx::mbar_wait(&bars[B_DS_EMPTY0 + sb], ((x / C::NDS) - 1) & 1);
 #pragma unroll
-            for (int c8 = 0; c8 < 4; ++c8) {
+            for (int c8 = 0; c8 < CH / 8; ++c8) {
               const uint32_t off = sw128_chunk_offset(128, row, (cc0 + c8 * 8) >> 3);
               *reinterpret_cast<uint4*>(pdS + off) =
                   make_uint4(dk2[c8 * 4], dk2[c8 * 4 + 1], dk2[c8 * 4 + 2], dk2[c8 * 4 + 3]);

@@ -13,7 +13,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdash.so")
+# DASH_LIB_PATH: an experiment build of the same library (scripts/build_variant.py)
+LIB_PATH = os.environ.get("DASH_LIB_PATH") or os.path.join(_HERE, "libdash.so")
 
 NAIVE, DESCENDING, SHIFT, AUTO = 0, 1, 2, 3
 FULL, CAUSAL = 0, 1

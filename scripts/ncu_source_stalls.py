@@ -28,7 +28,7 @@ for r in csv.reader(raw.splitlines()):
         except ValueError:
             s = 0.0
         st = {k[6:]: float(v) for k, v in d.items()
-              if k.startswith("stall_") and "(Not" not in k and v not in ("", "0")}
+              if k.startswith("stall_") and "(Not" not in k and v not in ("", "0", "-")}
         agg.append((s, cur, int(r[0]), r[1].strip()[:90], st))
 tot = sum(a[0] for a in agg) or 1.0
 print(f"# warp-stall samples per source line ({rep}); all files: {tot:.0f} samples")
