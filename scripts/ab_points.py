@@ -24,6 +24,8 @@ ap.add_argument("--seqlens", default="512,1024,2048,4096,8192,16384")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--tiles", default="0", help="dash_attn_bwd_set_tile values to compare (0 = library choice)")
 ap.add_argument("--rounds", type=int, default=1, help="interleaved rounds (median reported)")
+ap.add_argument("--splits", default="0", help="dash_attn_bwd_set_acc_split values to compare (0 = automatic)")
+ap.add_argument("--total", action="store_true", help="report K1 + K2 + K4 instead of the main kernel")
 args = ap.parse_args()
 res = {"tag": args.tag}
 for mask in args.masks.split(","):
@@ -34,8 +36,10 @@ for mask in args.masks.split(","):
         o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], causal)
         times = {}
         for _ in range(args.rounds):
-            for tile in (int(t) for t in args.tiles.split(",")):
+            for tile, wsplit in ((int(t), int(w)) for t in args.tiles.split(",")
+                                 for w in args.splits.split(",")):
                 dash.set_tile(tile)
+                dash.set_acc_split(wsplit)
                 for sched in args.scheds.split(","):
                     ws = dash.alloc_workspace(g["q"].shape, causal, sched, True, "cuda")
                     for _ in range(3):
@@ -47,10 +51,13 @@ for mask in args.masks.split(","):
                         dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal, sched, True,
                                       workspace=ws)
                     pre, main, post, n = dash.profile_end()
-                    key = f"{mask}/{sched}/{N}" + (f"/t{tile}" if tile else "")
-                    times.setdefault(key, []).append(1000 * main / n)  # us per call
+                    key = (f"{mask}/{sched}/{N}" + (f"/t{tile}" if tile else "") +
+                           (f"/W{wsplit}" if wsplit else ""))
+                    tot = (pre + main + post) if args.total else main
+                    times.setdefault(key, []).append(1000 * tot / n)  # us per call
                     del ws
         dash.set_tile(0)
+        dash.set_acc_split(0)
         for key, v in times.items():
             res[key] = round(sorted(v)[len(v) // 2], 1)
 print(json.dumps(res))
