@@ -47,6 +47,7 @@ struct BwdArgs {
   int* error_flag;       // 1
   const int* job_begin;  // [jobs_per_head + 1]
   const int2* tasks;     // {kv | q << 16, rank}
+  const int* seg_end;    // per task: index of the first task of the next KV segment (or job end)
   int B, N, H;
   int jobs_per_head;
   int total_jobs;
@@ -441,10 +442,8 @@ __global__ void __launch_bounds__(512, 1)
         const int t1 = __shfl_sync(0xffffffffu, jv.t1, 0);
         int ts = __shfl_sync(0xffffffffu, jv.t0, 0);
         while (ts < t1) {
-          const int seg = task_seg(args.tasks[ts]);
-          int te = ts + 1;
-          while (te < t1 && task_seg(args.tasks[te]) == seg) ++te;
-          te = __shfl_sync(0xffffffffu, te, 0);
+          // one table load (a scan over the tasks would chain L2 round trips)
+          const int te = __shfl_sync(0xffffffffu, args.seg_end[ts], 0);
           const uint32_t nsub = static_cast<uint32_t>(te - ts) * NSUB;
           ptx::mbar_wait_u(&bars[B_KV_FULL], kv_cnt & 1);
           ++kv_cnt;

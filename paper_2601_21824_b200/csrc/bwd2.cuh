@@ -269,9 +269,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
       };
       int ts = jv.t0;
       while (ts < jv.t1 && !ptx::aborted()) {
-        const int seg = task_seg(args.tasks[ts]);
-        int te = ts + 1;
-        while (te < jv.t1 && task_seg(args.tasks[te]) == seg) ++te;
+        const int te = args.seg_end[ts];  // one load, not a chain of L2 round trips
         const TaskView tv0 = decode_task(args, jv, args.tasks[ts]);
         // K / V of this KV segment: free once the previous segment's last
         // S^T / dP^T completed (KV_FREE) -- before its last softmax / dK / dV / dQ
@@ -440,10 +438,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
       const int t1 = __shfl_sync(0xffffffffu, jv.t1, 0);
       int ts = __shfl_sync(0xffffffffu, jv.t0, 0);
       while (ts < t1) {
-        const int seg = task_seg(args.tasks[ts]);
-        int te = ts + 1;
-        while (te < t1 && task_seg(args.tasks[te]) == seg) ++te;
-        te = __shfl_sync(0xffffffffu, te, 0);
+        const int te = __shfl_sync(0xffffffffu, args.seg_end[ts], 0);
         const uint32_t nsub = static_cast<uint32_t>(te - ts) * NSUB;
         ptx::mbar_wait_u(&bars[P_KV_FULL], kv_cnt & 1);
         ++kv_cnt;

@@ -314,6 +314,7 @@ int device_sms(int dev) {
 struct DevTable {
   int* job_begin = nullptr;
   int2* tasks = nullptr;
+  int* seg_end = nullptr;  // per task: first task of the next KV segment of its job
   int jobs = 0;
 };
 // With head grouping G (BwdArgs::head_group) job lj lists the tasks of the
@@ -335,15 +336,31 @@ const DevTable* device_table(int dev, const ScheduleTable* t, int G) {
                                t->tasks[i].rank | (hoff << 16)));
     jb.push_back(static_cast<int>(tk.size()));
   }
+  // Segment ends: a KV segment is a maximal run of tasks with the same (kv,
+  // head offset) -- the kernels' task_seg(); the kernels read te here instead
+  // of scanning the tasks.
+  std::vector<int> se(tk.size());
+  for (int lj = 0; lj < t->jobs; ++lj) {
+    const int b = jb[lj], e = jb[lj + 1];
+    for (int i = e - 1; i >= b; --i) {
+      const auto seg = [&](int k) {
+        return (tk[k].x & 0xFFFF) | (tk[k].y & static_cast<int>(0xFFFF0000u));
+      };
+      se[i] = (i + 1 < e && seg(i + 1) == seg(i)) ? se[i + 1] : i + 1;
+    }
+  }
   DevTable d;
   d.jobs = t->jobs;
   void* buf = nullptr;
   const size_t jb_bytes = align_up(jb.size() * sizeof(int), 256);
-  if (cudaMalloc(&buf, jb_bytes + tk.size() * sizeof(int2)) != cudaSuccess) return nullptr;
+  const size_t tk_bytes = align_up(tk.size() * sizeof(int2), 256);
+  if (cudaMalloc(&buf, jb_bytes + tk_bytes + se.size() * sizeof(int)) != cudaSuccess) return nullptr;
   d.job_begin = static_cast<int*>(buf);
   d.tasks = reinterpret_cast<int2*>(static_cast<char*>(buf) + jb_bytes);
+  d.seg_end = reinterpret_cast<int*>(static_cast<char*>(buf) + jb_bytes + tk_bytes);
   cudaMemcpy(d.job_begin, jb.data(), jb.size() * sizeof(int), cudaMemcpyHostToDevice);
   cudaMemcpy(d.tasks, tk.data(), tk.size() * sizeof(int2), cudaMemcpyHostToDevice);
+  cudaMemcpy(d.seg_end, se.data(), se.size() * sizeof(int), cudaMemcpyHostToDevice);
   cache[key] = d;
   return &cache[key];
 }
@@ -503,6 +520,7 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     a.error_flag = counters + 1;
     a.job_begin = dt->job_begin;
     a.tasks = dt->tasks;
+    a.seg_end = dt->seg_end;
     a.B = s->batch;
     a.N = s->seqlen;
     a.H = s->heads;
@@ -647,6 +665,7 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
     a.error_flag = counters + 1;
     a.job_begin = dt->job_begin;
     a.tasks = dt->tasks;
+    a.seg_end = dt->seg_end;
     a.B = s->batch;
     a.N = s->seqlen;
     a.H = s->heads;
