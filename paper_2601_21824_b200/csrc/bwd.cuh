@@ -354,19 +354,19 @@ __global__ void __launch_bounds__(512, 1)
             ++q_cnt;
           }
         }
-        // Every load of job g is issued and (KV_EMPTY) every MMA of g has
-        // completed: claim the next job now -- its K/V load can start at once --
-        // instead of after the last ordered add of g is released (measured:
-        // that tail costs ~18 k cycles per job).  Claiming as soon as the loads
-        // are issued was slower: the claimed job then waits several sub-tiles,
-        // which splits the co-scheduling of a SHIFT head.  Deadlock-free: a CTA
-        // holds at most one claimed-ahead job, queued behind g; g's remaining
-        // adds wait only on jobs of g's head, all claimed earlier.  With cyclic
-        // waits inside a head (SHIFT) the claimed-ahead job must belong to
-        // another head, so it is never in g's wait cycle; with acyclic waits
-        // (NAIVE, DESCENDING: rank = KV index, waits point to earlier-claimed
-        // jobs) any job is fine.  Otherwise reducer agent 0 claims as before.
-        if (args.prefetch) ptx::mbar_wait_u(&bars[B_KV_EMPTY], (kv_cnt - 1) & 1);
+        // Every load of job g is issued: claim the next job now -- its claim
+        // (an atomic that all CTAs of a SHIFT wave issue together, ~3 k cycles)
+        // and its K/V load overlap g's last sub-tiles -- instead of after the
+        // last ordered add of g is released (~18 k cycles per job, round 1).
+        // Measured (profiles/r02_experiments_early_claim.txt): claiming here
+        // beats waiting for g's MMAs (KV_EMPTY) by 1-5 %, once the claim itself
+        // is a single atomic.  Deadlock-free: a CTA holds at most one
+        // claimed-ahead job, queued behind g; g's remaining adds wait only on
+        // jobs of g's head, all claimed earlier.  With cyclic waits inside a
+        // head (SHIFT) the claimed-ahead job must belong to another head, so it
+        // is never in g's wait cycle; with acyclic waits (NAIVE, DESCENDING:
+        // rank = KV index, waits point to earlier-claimed jobs) any job is
+        // fine.  Otherwise reducer agent 0 claims as before.
         if (lane == 0) {
           int mode = 2;
           wait_slot_free(it_job);  // slot it_job % 2 / claim_mode slot reusable

@@ -315,10 +315,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
         ts = te;
       }
       // Claim of the next job (leader only) -- as in bwd.cuh: early claim
-      // (prefetch) once every MMA of g has completed, else reducer agent 0
+      // (prefetch) once every load of g is issued, else reducer agent 0
       // claims after the last release.
       if (leader) {
-        if (args.prefetch) ptx::mbar_wait_u(&bars[P_KV_EMPTY], (kv_cnt - 1) & 1);
         if (lane == 0) {
           DASH_TRACE_MARK(28, q_cnt);
           int mode = 2;
