@@ -302,6 +302,10 @@ __global__ void __launch_bounds__(512, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  // The prologue above overlaps the preprocess kernel's tail (programmatic
+  // dependent launch); D, lse2, tickets and the job counter are read only now.
+  ptx::griddep_launch();
+  ptx::griddep_wait();
 
   const int n_units = args.N / C::STG_ROWS;  // tickets per head (one per staging unit)
 
@@ -897,6 +901,8 @@ __global__ void __launch_bounds__(256) dash_preprocess_kernel(
     size_t n_zero_f4, int* __restrict__ counters, int poison) {
   constexpr int T = D / 8;      // threads per row, 16 B each
   constexpr int RPB = 256 / T;  // rows per block and half-iteration
+  ptx::griddep_wait();    // the previous call's kernels may still read this workspace
+  ptx::griddep_launch();  // the main kernel's prologue may start on SMs this grid leaves
   const size_t rows = static_cast<size_t>(B) * N * H;
   const int part = static_cast<int>(threadIdx.x % T);
   auto row_addr = [&](size_t r) { return r * D + part * 8; };  // r = (b*N + n)*H + h
@@ -975,6 +981,8 @@ __global__ void __launch_bounds__(256) dash_dq_convert_kernel(
     const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq, int N, int H, float scale,
     int causal, int tile, int bh_base, int bh_count) {
   constexpr int T = D / 8;
+  ptx::griddep_wait();  // every ordered add of the main kernel has landed
+  ptx::griddep_launch();
   const size_t total = static_cast<size_t>(bh_count) * N * T;
   const size_t plane = static_cast<size_t>(bh_count) * N * D;
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;

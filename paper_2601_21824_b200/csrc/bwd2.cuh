@@ -206,6 +206,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
   ptx::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
   ptx::tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  // The prologue above overlaps the preprocess kernel's tail (programmatic
+  // dependent launch); D, lse2, tickets and the job counter are read only now.
+  ptx::griddep_launch();
+  ptx::griddep_wait();
   const int n_units = args.N / BR;  // Q sub-tiles per head
 
   if (warp == 0) {

@@ -411,6 +411,22 @@ cudaError_t reset_chunk(char* ws, const WsLayout& w, int deterministic, cudaStre
   return e;
 }
 
+// Programmatic dependent launch between the call's kernels (K1 -> K2 -> K4):
+// each kernel waits (griddepcontrol.wait) before touching what its
+// predecessor writes, so its launch and prologue overlap the predecessor's
+// tail.  DASH_PDL=0 turns the attribute off (experiments).
+bool pdl_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("DASH_PDL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+void set_pdl(cudaLaunchAttribute* a) {
+  a->id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a->val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+}
+
 // K1 and K4 grids: one wave of 256-thread blocks (8 per SM), grid-stride.
 template <int D>
 void launch_preprocess(const dash_shape* s, const void* o, const void* dout, const float* lse,
@@ -420,10 +436,18 @@ void launch_preprocess(const dash_shape* s, const void* o, const void* dout, con
   const size_t rows = static_cast<size_t>(s->batch) * s->seqlen * s->heads;
   size_t g = (rows + 2 * RPB - 1) / (2 * RPB);
   if (g > static_cast<size_t>(sms) * 8) g = static_cast<size_t>(sms) * 8;
-  dash_preprocess_kernel<D><<<static_cast<unsigned>(g), 256, 0, stream>>>(
-      static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse, dvec, lse2,
-      s->batch, s->seqlen, s->heads, tickets, n_tickets, reinterpret_cast<float4*>(zero), n_zero_f4,
-      counters, poison);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(g));
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  set_pdl(&attr[0]);
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, dash_preprocess_kernel<D>, static_cast<const __nv_bfloat16*>(o),
+                     static_cast<const __nv_bfloat16*>(dout), lse, dvec, lse2, s->batch, s->seqlen,
+                     s->heads, tickets, n_tickets, reinterpret_cast<float4*>(zero), n_zero_f4,
+                     counters, poison);
 }
 template <int D>
 void launch_convert(const dash_shape* s, const float* dqacc, void* dq, int W, int causal, int tile,
@@ -431,16 +455,22 @@ void launch_convert(const dash_shape* s, const float* dqacc, void* dq, int W, in
   const size_t total = static_cast<size_t>(bh_count) * s->seqlen * (D / 8);
   size_t g = (total + 2 * 256 - 1) / (2 * 256);
   if (g > static_cast<size_t>(sms) * 8) g = static_cast<size_t>(sms) * 8;
-  const dim3 grid(static_cast<unsigned>(g));
   auto* out = static_cast<__nv_bfloat16*>(dq);
   const float sc = eff_scale(s);
   const int c = causal ? 1 : 0;
-  switch (W) {
-    case 1: dash_dq_convert_kernel<D, 1><<<grid, 256, 0, stream>>>(dqacc, out, s->seqlen, s->heads, sc, c, tile, bh_base, bh_count); break;
-    case 2: dash_dq_convert_kernel<D, 2><<<grid, 256, 0, stream>>>(dqacc, out, s->seqlen, s->heads, sc, c, tile, bh_base, bh_count); break;
-    case 4: dash_dq_convert_kernel<D, 4><<<grid, 256, 0, stream>>>(dqacc, out, s->seqlen, s->heads, sc, c, tile, bh_base, bh_count); break;
-    default: dash_dq_convert_kernel<D, 8><<<grid, 256, 0, stream>>>(dqacc, out, s->seqlen, s->heads, sc, c, tile, bh_base, bh_count); break;
-  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(g));
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  set_pdl(&attr[0]);
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  auto kern = W == 1 ? dash_dq_convert_kernel<D, 1>
+              : W == 2 ? dash_dq_convert_kernel<D, 2>
+              : W == 4 ? dash_dq_convert_kernel<D, 4>
+                       : dash_dq_convert_kernel<D, 8>;
+  cudaLaunchKernelEx(&cfg, kern, dqacc, out, s->seqlen, s->heads, sc, c, tile, bh_base, bh_count);
 }
 
 template <int D>
@@ -550,11 +580,12 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
       cfg.blockDim = dim3(C::NTHREADS);
       cfg.dynamicSmemBytes = C::SMEM_BYTES;
       cfg.stream = stream;
-      cudaLaunchAttribute attr[1];
+      cudaLaunchAttribute attr[2];
       attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for SHIFT (AMB-12)
       attr[0].val.cooperative = 1;
+      set_pdl(&attr[1]);
       cfg.attrs = attr;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = 2;
       const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tdo, tacc, tdk, tdv, a);
       if (le != cudaSuccess) {
         g_last_cuda = 10000 + static_cast<int>(le);  // launch of the main kernel
@@ -694,6 +725,10 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
       cfg.blockDim = dim3(C::NTHREADS);
       cfg.dynamicSmemBytes = C::SMEM_BYTES;
       cfg.stream = stream;
+      cudaLaunchAttribute attr[1];
+      set_pdl(&attr[0]);
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
       const cudaError_t le =
           cudaLaunchKernelEx(&cfg, kern, tq32, tq64, tk, tv, tdo32, tdo64, tacc, tdk, tdv, a);
       if (le != cudaSuccess) {
