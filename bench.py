@@ -700,7 +700,8 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": dash.bwd_launches(causal, args.schedule, True) * len(full_shapes) * args.steps,
+            "gpu_launches": sum(dash.bwd_launch_count(sh, causal, args.schedule, True)
+                                for sh in full_shapes) * args.steps,
             "clocks": clk.summary(),
             "sharding_bitwise_identical": sharding_ok,
             "gate": gate,

@@ -304,9 +304,28 @@ dash_status dash_attn_bwd_set_tile(int tile);
 dash_status dash_attn_bwd_set_plane_budget(size_t bytes);
 int dash_attn_bwd_head_chunk(const dash_shape* shape, int causal, int schedule, int deterministic);
 
-/* Number of device kernel launches one dash_attn_bwd makes (for accounting):
- * 3 (preprocess, main, dQ convert) when the heads fit one chunk (see
- * dash_attn_bwd_head_chunk), else 1 + 2 * chunks. */
+/* dQ finalise (the fp32 accumulator of P:396 turned into
+ * the bf16 dQ output).  mode 1 (default): from N = 2048 the main kernel
+ * writes dq itself -- every reducer agent counts its completed jobs (release)
+ * and CTAs whose jobs ran out convert the heads whose jobs all completed
+ * (acquire), in the kernel's tail -- and below N = 2048 (short jobs, little
+ * tail; measured faster there) the separate K4 convert kernel does.  mode 0:
+ * always K4; mode 2: always in the main kernel.  Every mode forms
+ * bf16(scale * (acc_0 + ... + acc_{W-1})) in the same order: results are
+ * bit-identical.  Host-global, later calls; the workspace size does not
+ * depend on it.  DASH_ERR_INVALID_ARG for another mode. */
+dash_status dash_attn_bwd_set_fused_dq(int mode);
+int dash_attn_bwd_fused_dq(void);
+
+/* Device kernel launches one dash_attn_bwd with these arguments makes: 1
+ * (preprocess) + per chunk of heads (dash_attn_bwd_head_chunk) the main
+ * kernel and, unless the dQ finalise is fused for this shape, K4.  0 for an
+ * invalid shape or schedule. */
+int dash_attn_bwd_launch_count(const dash_shape* shape, int causal, int schedule,
+                               int deterministic);
+
+/* Shape-free form: 3 (preprocess, main, dQ convert), or 2 when the finalise
+ * is always fused (mode 2), for heads that fit one chunk. */
 int dash_attn_bwd_launches(int causal, int schedule, int deterministic);
 
 /* Diagnostic code behind the calling thread's most recent DASH_ERR_CUDA (0 if

@@ -86,6 +86,19 @@ struct BwdArgs {
   // unless the planes of all heads exceed the budget.
   int bh_base;
   int bh_count;
+  // Fused dQ finalise: the main kernel writes dq
+  // itself, so there is no K4.  Every reducer agent adds 1 to done[g /
+  // jobs_per_head] (release, after its job's last ordered add completed); once
+  // a job group's count reaches jobs_per_head x agents all of its heads' dQ
+  // accumulators are final.  CTAs that find the job counter exhausted then
+  // claim finalise tasks (done[bh_count / head_group] is the task counter,
+  // 64 / 128 rows of one head per task, heads in job order) and write
+  // dq = bf16(scale * (acc_0 + ... + acc_{W-1})), the sum K4 forms.
+  int* done;
+  __nv_bfloat16* dq;  // [B,N,H,d]
+  int fuse_dq;        // 0: K4 converts (dash_attn_bwd_set_fused_dq(0))
+  int acc_tile;       // schedule tile rows (128 / 256): contributions per Q tile
+  int done_target;    // jobs_per_head x reducer agents per job (both CTAs of a pair)
 };
 
 // Per-(CTA, sub-tile) clock64 stamps for pipeline analysis; a null trace
@@ -241,6 +254,131 @@ __device__ __forceinline__ TaskView decode_task(const BwdArgs& a, const JobView&
   v.h = v.bh % a.H;
   v.seg = task_seg(tk);
   return v;
+}
+
+// Reducer agent: this job's ordered adds are complete -- count it (the bulk
+// groups were waited on with wait_group 0; the proxy fence orders the async
+// proxy's writes before the generic release).
+__device__ __forceinline__ void count_job_done(const BwdArgs& a, int g) {
+  if (!a.fuse_dq) return;
+  ptx::fence_async_global();
+  ptx::red_release_add(a.done + g / a.jobs_per_head, 1);
+}
+
+// Fused dQ finalise, run by every thread of a CTA after its roles found no
+// job left.  `slot` = one int of shared memory.  Tasks are claimed in head
+// order (the order heads complete in); a task waits (acquire) for its job
+// group's completion count.  Per element the arithmetic is K4's: the planes a
+// Q tile was written into, added in index order, times scale, to bf16.
+template <int D, int NT, int W>
+__device__ __forceinline__ void finalize_dq_w(const BwdArgs& a, int* slot) {
+  constexpr int T = D / 8;             // threads per row, 8 elements each
+  constexpr int RPP = NT / T;          // rows per pass
+  constexpr int FR = 16384 / D;        // rows per task (64 KB of fp32 per plane)
+  constexpr int PASSES = FR / RPP;
+  constexpr int UMAX = W <= 2 ? 4 : (W == 4 ? 2 : 1);
+  constexpr int U = PASSES < UMAX ? PASSES : UMAX;  // passes with their loads in flight together
+  static_assert(PASSES % U == 0, "passes");
+  const int tid = threadIdx.x;
+  const int nrb = (a.N + FR - 1) / FR;  // d = 64: N may end in half a task
+  const int G = a.head_group;
+  const int total = a.bh_count * nrb;
+  int* task_counter = a.done + a.bh_count / G;
+  const size_t plane = static_cast<size_t>(a.bh_count) * a.N * D;
+  const int part = tid % T;
+  auto group_done = [&](int task) { return a.done + (task / nrb) / G; };
+  // Thread 0 claims one task ahead and, while the current task's loads are in
+  // flight, checks (acquire) whether the next task's job group is complete, so
+  // a finished group costs no round trip at the start of its task.  Abort
+  // decisions are thread 0's, read back by all: uniform at every barrier.
+  bool ready = false;
+  if (tid == 0) slot[0] = ptx::aborted() ? total : atomicAdd(task_counter, 1);
+  __syncthreads();
+  int t = slot[0];
+  while (t < total) {
+    const int lh = t / nrb, rb = t % nrb;  // local head, row block
+    int nxt = 0;
+    if (tid == 0) {
+      nxt = atomicAdd(task_counter, 1);
+      const int* cnt = group_done(t);
+      if (!ready && ptx::ld_acquire(cnt) < a.done_target) {
+        const long long t0 = clock64();
+        uint32_t polls = 0;
+        while (ptx::ld_relaxed(cnt) < a.done_target) {
+          __nanosleep(64);
+          if ((++polls & ptx::kAbortPollMask) != 0) continue;
+          if (clock64() - t0 > a.spin_bound || ptx::aborted()) {
+            atomicExch(a.error_flag, 1);
+            atomicExch(&ptx::g_dash_abort, 1);
+            break;
+          }
+        }
+        (void)ptx::ld_acquire(cnt);
+      }
+      ptx::fence_async_global();
+      slot[2] = ptx::aborted() ? 1 : 0;
+    }
+    __syncthreads();
+    if (slot[2]) break;
+    const int bh = a.bh_base + lh;
+    const int h = bh % a.H, b = bh / a.H;
+#pragma unroll
+    for (int u0 = 0; u0 < PASSES; u0 += U) {
+      float4 x[U][W][2];
+      int planes[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int n = rb * FR + (u0 + u) * RPP + tid / T;
+        const int cnt = a.causal ? n / a.acc_tile + 1 : a.N / a.acc_tile;
+        planes[u] = n >= a.N ? 0 : (W < cnt ? W : cnt);  // accumulator w holds ranks w, w + W, ...
+        const float* src = a.dqacc + (static_cast<size_t>(lh) * a.N + n) * D + part * 8;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          if (w < planes[u]) {
+            x[u][w][0] = __ldcs(reinterpret_cast<const float4*>(src + w * plane));
+            x[u][w][1] = __ldcs(reinterpret_cast<const float4*>(src + w * plane + 4));
+          }
+        }
+      }
+      if (tid == 0 && u0 == 0) {
+        slot[1] = nxt;
+        ready = nxt < total && ptx::ld_acquire(group_done(nxt)) >= a.done_target;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int n = rb * FR + (u0 + u) * RPP + tid / T;
+        if (planes[u] == 0) continue;
+        float4 s0 = x[u][0][0], s1 = x[u][0][1];
+#pragma unroll
+        for (int w = 1; w < W; ++w) {
+          if (w < planes[u]) {
+            s0 = make_float4(s0.x + x[u][w][0].x, s0.y + x[u][w][0].y, s0.z + x[u][w][0].z,
+                             s0.w + x[u][w][0].w);
+            s1 = make_float4(s1.x + x[u][w][1].x, s1.y + x[u][w][1].y, s1.z + x[u][w][1].z,
+                             s1.w + x[u][w][1].w);
+          }
+        }
+        uint4 out;
+        out.x = pack_bf16(s0.x * a.scale, s0.y * a.scale);
+        out.y = pack_bf16(s0.z * a.scale, s0.w * a.scale);
+        out.z = pack_bf16(s1.x * a.scale, s1.y * a.scale);
+        out.w = pack_bf16(s1.z * a.scale, s1.w * a.scale);
+        *reinterpret_cast<uint4*>(a.dq + ((static_cast<size_t>(b) * a.N + n) * a.H + h) * D +
+                                  part * 8) = out;
+      }
+    }
+    __syncthreads();  // slot[1] published; slot[1] / slot[2] rewritten only after the next barrier
+    t = slot[1];
+  }
+}
+template <int D, int NT>
+__device__ __forceinline__ void finalize_dq(const BwdArgs& a, int* slot) {
+  switch (a.split) {
+    case 1: finalize_dq_w<D, NT, 1>(a, slot); break;
+    case 2: finalize_dq_w<D, NT, 2>(a, slot); break;
+    case 4: finalize_dq_w<D, NT, 4>(a, slot); break;
+    default: finalize_dq_w<D, NT, 8>(a, slot); break;
+  }
 }
 
 template <int D>
@@ -616,6 +754,7 @@ __global__ void __launch_bounds__(512, 1)
         }
         // Every agent has released every add of this job: only now may the
         // CTA claim its next job (greedy claiming of AMB-7, deadlock-free).
+        count_job_done(args, g);
         ptx::mbar_arrive(&bars[B_JOB_DONE]);
         if (agent == 0) {
           ptx::mbar_wait(&bars[B_JOB_DONE], it_job & 1);
@@ -882,6 +1021,7 @@ __global__ void __launch_bounds__(512, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tbase);
   }
+  if (args.fuse_dq) finalize_dq<D, C::NTHREADS>(args, reinterpret_cast<int*>(smem + C::OFF_DQ));
   if (tid == 0 && ptx::aborted()) atomicExch(args.error_flag, 2);
 }
 

@@ -570,6 +570,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
             DASH_TRACE_MARK(9, x);
           }
         }
+        count_job_done(args, g);
         ptx::mbar_arrive_remote(lbar(P_JOB_DONE));
         if (leader && agent == 0) {
           ptx::mbar_wait_cluster(&bars[P_JOB_DONE], it_job & 1);
@@ -842,6 +843,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc2<512>(tbase);
   }
+  if (args.fuse_dq) finalize_dq<D, C::NTHREADS>(args, reinterpret_cast<int*>(smem + C::OFF_DQ));
   if (tid == 0 && ptx::aborted()) atomicExch(args.error_flag, 2);
 }
 

@@ -204,7 +204,8 @@ constexpr size_t kDefaultPlaneBudget = size_t(4) << 30;
 size_t g_plane_budget = kDefaultPlaneBudget;
 
 struct WsLayout {
-  size_t dqacc = 0, dvec = 0, lse2 = 0, tickets = 0, counters = 0, total = 0;
+  size_t dqacc = 0, dvec = 0, lse2 = 0, tickets = 0, done = 0, counters = 0, total = 0;
+  size_t n_done = 0;  // fused dQ finalise: job-group completion counts + the task counter
   size_t dqacc_bytes = 0, n_tickets = 0;  // per accumulator, for one chunk of heads
   int planes = 1;
   int chunk = 1, chunks = 1;  // heads per chunk, number of chunks
@@ -235,8 +236,11 @@ WsLayout ws_layout(const dash_shape* s, int W, int G = 1) {
   w.lse2 = off;
   off = align_up(off + BHN * 4, kAlign);
   w.tickets = off;
-  off = align_up(off + static_cast<size_t>(W) * w.n_tickets * 4, kAlign);
-  w.counters = off;  // [0] job counter, [1] error flag (directly after the tickets)
+  // done[] follows the tickets directly: K1 and reset_chunk zero both in one range
+  w.done = off + static_cast<size_t>(W) * w.n_tickets * 4;
+  w.n_done = static_cast<size_t>(w.chunk) + 1;
+  off = align_up(w.done + w.n_done * 4, kAlign);
+  w.counters = off;  // [0] job counter, [1] error flag (directly after done[])
   off = align_up(off + 64, kAlign);
   w.total = off;
   return w;
@@ -247,6 +251,17 @@ WsLayout layout_for(const dash_shape* s, int deterministic, int causal, int sche
   const int sch = resolve_sched(s, causal, schedule);
   const int G = tile_for(s, causal, sch) == PairCfg::TILE ? 1 : head_group_for(s);
   return ws_layout(s, resolved_split(s, deterministic, causal, schedule), G);
+}
+
+// dQ finalise (dash_attn_bwd_set_fused_dq): 0 = the separate K4 convert, 1 =
+// in the main kernel from N = 2048 (default), 2 = always in the main kernel.
+// Both form the same sums.  The in-kernel finalise runs on CTAs whose jobs ran
+// out, so it hides in the kernel's tail; heads shorter than 2048 rows have
+// short jobs and little tail, and there K4 (2048 threads per SM against the
+// main kernel's 512) measured faster (profiles/r02_experiments_fused_dq.txt).
+int g_fused_dq = 1;
+bool fused_for(const dash_shape* s) {
+  return g_fused_dq == 2 || (g_fused_dq == 1 && s->seqlen >= 2048);
 }
 
 // Ticket-wait watchdog (clock64 cycles): default ~35 s at 1.965 GHz.
@@ -533,7 +548,8 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
   g_poison = 0;
   prof_mark(stream, 0);
   // K1: D, ticket / counter / error-flag reset, dQacc zero-fill for the atomic variant.
-  launch_preprocess<D>(s, o, dout, lse, dvec, lse2, tickets, static_cast<int>(W * w.n_tickets),
+  launch_preprocess<D>(s, o, dout, lse, dvec, lse2, tickets,
+                       static_cast<int>(W * w.n_tickets + w.n_done),
                        deterministic ? nullptr : dqacc, deterministic ? 0 : w.dqacc_bytes / 16,
                        counters, poison, sms, stream);
   prof_mark(stream, 1);
@@ -569,6 +585,11 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
     a.prefetch = early_claim(schedule, causal, deterministic, W, false, tab->jobs);
     a.cyclic = (deterministic && schedule == kShift) ? 1 : 0;
     a.head_group = G;
+    a.done = reinterpret_cast<int*>(ws + w.done);
+    a.dq = static_cast<__nv_bfloat16*>(dq);
+    a.fuse_dq = fused_for(s) ? 1 : 0;
+    a.acc_tile = 128;
+    a.done_target = tab->jobs * NAG;
     const int BH = s->batch * s->heads;
     for (int c = 0; c < w.chunks; ++c) {
       a.bh_base = c * w.chunk;
@@ -592,8 +613,9 @@ dash_status launch_bwd(const dash_shape* s, const void* q, const void* k, const 
         return DASH_ERR_CUDA;
       }
       prof_mark(stream, 2);
-      // K4: dQ = bf16(scale * (acc_0 + ... + acc_{W-1})) for the chunk's heads.
-      launch_convert<D>(s, dqacc, dq, W, causal, 128, a.bh_base, a.bh_count, sms, stream);
+      // K4: dQ = bf16(scale * (acc_0 + ... + acc_{W-1})) for the chunk's heads
+      // (unless the main kernel finalised dQ itself).
+      if (!a.fuse_dq) launch_convert<D>(s, dqacc, dq, W, causal, 128, a.bh_base, a.bh_count, sms, stream);
       prof_mark(stream, 3);
     }
   }
@@ -681,7 +703,8 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
   g_poison = 0;
   prof_mark(stream, 0);
   // K1: D, ticket / counter / error-flag reset, dQacc zero-fill for the atomic variant.
-  launch_preprocess<D>(s, o, dout, lse, dvec, lse2, tickets, static_cast<int>(W * w.n_tickets),
+  launch_preprocess<D>(s, o, dout, lse, dvec, lse2, tickets,
+                       static_cast<int>(W * w.n_tickets + w.n_done),
                        deterministic ? nullptr : dqacc, deterministic ? 0 : w.dqacc_bytes / 16,
                        counters, poison, sms, stream);
   prof_mark(stream, 1);
@@ -715,6 +738,11 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
     a.prefetch = early_claim(schedule, causal, deterministic, W, true, tab->jobs);
     a.cyclic = (deterministic && schedule == kShift) ? 1 : 0;
     a.head_group = 1;
+    a.done = reinterpret_cast<int*>(ws + w.done);
+    a.dq = static_cast<__nv_bfloat16*>(dq);
+    a.fuse_dq = fused_for(s) ? 1 : 0;
+    a.acc_tile = C::TILE;
+    a.done_target = tab->jobs * 2 * NAG;  // both CTAs' agents
     for (int c = 0; c < w.chunks; ++c) {
       a.bh_base = c * w.chunk;
       a.bh_count = std::min(w.chunk, BH - a.bh_base);
@@ -736,7 +764,8 @@ dash_status launch_bwd_pair(const dash_shape* s, const void* q, const void* k, c
         return DASH_ERR_CUDA;
       }
       prof_mark(stream, 2);
-      launch_convert<D>(s, dqacc, dq, W, causal, C::TILE, a.bh_base, a.bh_count, sms, stream);
+      if (!a.fuse_dq)
+        launch_convert<D>(s, dqacc, dq, W, causal, C::TILE, a.bh_base, a.bh_count, sms, stream);
       prof_mark(stream, 3);
     }
   }
@@ -799,11 +828,25 @@ DASH_API dash_status dash_profile_end(double* ms_pre, double* ms_main, double* m
   return DASH_OK;
 }
 
+DASH_API dash_status dash_attn_bwd_set_fused_dq(int on) {
+  if (on < 0 || on > 2) return DASH_ERR_INVALID_ARG;
+  g_fused_dq = on;
+  return DASH_OK;
+}
+DASH_API int dash_attn_bwd_fused_dq(void) { return g_fused_dq; }
+
 DASH_API int dash_attn_bwd_launches(int causal, int schedule, int deterministic) {
   (void)causal;
   (void)schedule;
   (void)deterministic;
-  return 3;  // preprocess, main, dQ convert
+  return g_fused_dq == 2 ? 2 : 3;  // preprocess, main (+ dQ convert)
+}
+
+DASH_API int dash_attn_bwd_launch_count(const dash_shape* shape, int causal, int schedule,
+                                        int deterministic) {
+  if (!shape_ok(shape) || schedule < DASH_SCHED_NAIVE || schedule > DASH_SCHED_AUTO) return 0;
+  const WsLayout w = layout_for(shape, deterministic, causal, schedule);
+  return 1 + w.chunks * (fused_for(shape) ? 1 : 2);
 }
 
 namespace dash {

@@ -102,6 +102,12 @@ def _load():
     lib.dash_attn_bwd_set_plane_budget.argtypes = [ctypes.c_size_t]
     lib.dash_attn_bwd_head_chunk.restype = i
     lib.dash_attn_bwd_head_chunk.argtypes = [SP, i, i, i]
+    lib.dash_attn_bwd_set_fused_dq.restype = st
+    lib.dash_attn_bwd_set_fused_dq.argtypes = [i]
+    lib.dash_attn_bwd_fused_dq.restype = i
+    lib.dash_attn_bwd_fused_dq.argtypes = []
+    lib.dash_attn_bwd_launch_count.restype = i
+    lib.dash_attn_bwd_launch_count.argtypes = [SP, i, i, i]
     return lib
 
 
@@ -227,6 +233,24 @@ def acc_split(shape_bnhd=None, causal: bool = True, schedule="auto") -> int:
 def set_acc_split(w: int):
     """dash_attn_bwd_set_acc_split (host-global)."""
     _check(_lib.dash_attn_bwd_set_acc_split(int(w)), "dash_attn_bwd_set_acc_split")
+
+
+def set_fused_dq(mode: int):
+    """dash_attn_bwd_set_fused_dq (host-global): 0 = K4 convert kernel, 1 = in the main
+    kernel from N = 2048 (default), 2 = always in the main kernel."""
+    _check(_lib.dash_attn_bwd_set_fused_dq(int(mode)), "dash_attn_bwd_set_fused_dq")
+
+
+def fused_dq() -> int:
+    return int(_lib.dash_attn_bwd_fused_dq())
+
+
+def bwd_launch_count(shape_bnhd, causal=True, schedule="auto", deterministic=True) -> int:
+    """dash_attn_bwd_launch_count: device launches of one dash_attn_bwd with these arguments."""
+    B, N, H, d = shape_bnhd
+    shp = Shape(B, N, H, d, 0.0)
+    return int(_lib.dash_attn_bwd_launch_count(ctypes.byref(shp), int(causal), _sched(schedule),
+                                               int(deterministic)))
 
 
 def set_plane_budget(nbytes: int):

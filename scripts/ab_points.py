@@ -26,6 +26,7 @@ ap.add_argument("--tiles", default="0", help="dash_attn_bwd_set_tile values to c
 ap.add_argument("--rounds", type=int, default=1, help="interleaved rounds (median reported)")
 ap.add_argument("--splits", default="0", help="dash_attn_bwd_set_acc_split values to compare (0 = automatic)")
 ap.add_argument("--total", action="store_true", help="report K1 + K2 + K4 instead of the main kernel")
+ap.add_argument("--fused", default="1", help="dash_attn_bwd_set_fused_dq modes to compare (0 = K4, 1 = library choice, 2 = in-kernel)")
 args = ap.parse_args()
 res = {"tag": args.tag}
 for mask in args.masks.split(","):
@@ -36,8 +37,9 @@ for mask in args.masks.split(","):
         o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], causal)
         times = {}
         for _ in range(args.rounds):
-            for tile, wsplit in ((int(t), int(w)) for t in args.tiles.split(",")
-                                 for w in args.splits.split(",")):
+            for tile, wsplit, fz in ((int(t), int(w), int(f)) for t in args.tiles.split(",")
+                                     for w in args.splits.split(",") for f in args.fused.split(",")):
+                dash.set_fused_dq(fz)
                 dash.set_tile(tile)
                 dash.set_acc_split(wsplit)
                 for sched in args.scheds.split(","):
@@ -52,12 +54,13 @@ for mask in args.masks.split(","):
                                       workspace=ws)
                     pre, main, post, n = dash.profile_end()
                     key = (f"{mask}/{sched}/{N}" + (f"/t{tile}" if tile else "") +
-                           (f"/W{wsplit}" if wsplit else ""))
+                           (f"/W{wsplit}" if wsplit else "") + ("" if fz == 1 else f"/fz{fz}"))
                     tot = (pre + main + post) if args.total else main
                     times.setdefault(key, []).append(1000 * tot / n)  # us per call
                     del ws
         dash.set_tile(0)
         dash.set_acc_split(0)
+        dash.set_fused_dq(1)
         for key, v in times.items():
             res[key] = round(sorted(v)[len(v) // 2], 1)
 print(json.dumps(res))

@@ -4,6 +4,7 @@ sys.path.insert(0, os.getcwd())
 import torch
 from paper_2601_21824_b200 import dash
 from paper_2601_21824_b200.inputs import attn_inputs
+dash.set_fused_dq(int(os.environ.get("FUSED", "1")))
 SEQ = (512, 1024, 2048, 4096, 8192, 16384)
 probs = []
 for N in SEQ:

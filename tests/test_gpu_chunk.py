@@ -86,13 +86,16 @@ def test_chunked_atomic_variant_matches_oracle(dash):
         assert e <= 1e-2, (n, e)
 
 
-def test_profile_counts_chunked_launches(dash):
-    """dash_profile_end sums the main-kernel intervals of every chunk."""
+@pytest.mark.parametrize("fused", [True, False])
+def test_profile_counts_chunked_launches(dash, fused):
+    """dash_profile_end sums the main-kernel intervals of every chunk (and the
+    K4 intervals when the dQ finalise is not fused)."""
     B, N, H, d, causal = 1, 2048, 4, 128, True
     cpu = attn_inputs(B, N, H, d, seed=13)
     g = {k: v.cuda() for k, v in cpu.items()}
     g["o"], g["lse"] = dash.attn_fwd(g["q"], g["k"], g["v"], causal)
     dash.set_plane_budget(1)
+    dash.set_fused_dq(2 if fused else 0)
     try:
         ws = dash.alloc_workspace((B, N, H, d), causal, "auto", True, "cuda")
         dash.profile_begin()
@@ -100,6 +103,11 @@ def test_profile_counts_chunked_launches(dash):
             dash.attn_bwd(g["q"], g["k"], g["v"], g["o"], g["do"], g["lse"], causal, "auto", True,
                           workspace=ws)
         pre, main, post, calls = dash.profile_end()
+        launches = dash.bwd_launch_count((B, N, H, d), causal, "auto", True)
     finally:
         dash.set_plane_budget(0)
-    assert calls == 2 and pre > 0 and main > 0 and post > 0
+        dash.set_fused_dq(1)
+    assert calls == 2 and pre > 0 and main > 0 and post >= 0
+    if not fused:
+        assert post > 0
+    assert launches == 1 + H * (1 if fused else 2)  # one head per chunk
