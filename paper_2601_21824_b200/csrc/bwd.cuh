@@ -832,6 +832,7 @@ __global__ void __launch_bounds__(512, 1)
             // P = exp2(S*scale*log2e - L*log2e), dS = P o (dP - D), packed to bf16.
             // The causal mask (key row > query row) exists only on the diagonal
             // task; off the diagonal the per-element compare/select is skipped.
+            const unsigned long long sc2 = ptx::f2_pack(args.scale_log2, args.scale_log2);
             auto smx = [&](auto masked) {
               constexpr bool MASKED = decltype(masked)::value;
               const int mask_from = row - sub * BR - cc0;  // masked: cols c < mask_from
@@ -842,15 +843,25 @@ __global__ void __launch_bounds__(512, 1)
                 const float Lv[4] = {l4.x, l4.y, l4.z, l4.w};
                 const float Dv[4] = {d4.x, d4.y, d4.z, d4.w};
                 float p[4], ds[4];
+                // pairs of columns in packed fp32 (FFMA2 / FADD2 / FMUL2): the
+                // same roundings as fmaf(s, scale, L), dp - D, P * (.)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
+                for (int e = 0; e < 4; e += 2) {
                   const int c = c4 * 4 + e;
-                  float pv = fast_exp2(fmaf(s[c], args.scale_log2, Lv[e]));
+                  float t0, t1;
+                  ptx::f2_unpack(ptx::f2_fma(ptx::f2_pack(s[c], s[c + 1]), sc2,
+                                             ptx::f2_pack(Lv[e], Lv[e + 1])), t0, t1);
+                  float p0 = fast_exp2(t0), p1 = fast_exp2(t1);
                   if constexpr (MASKED) {
-                    if (c < mask_from) pv = 0.f;
+                    if (c < mask_from) p0 = 0.f;
+                    if (c + 1 < mask_from) p1 = 0.f;
                   }
-                  p[e] = pv;
-                  ds[e] = pv * (dp[c] - Dv[e]);
+                  p[e] = p0;
+                  p[e + 1] = p1;
+                  ptx::f2_unpack(ptx::f2_mul(ptx::f2_pack(p0, p1),
+                                             ptx::f2_sub(ptx::f2_pack(dp[c], dp[c + 1]),
+                                                         ptx::f2_pack(Dv[e], Dv[e + 1]))),
+                                 ds[e], ds[e + 1]);
                 }
                 pk[c4 * 2] = pack_bf16(p[0], p[1]);
                 pk[c4 * 2 + 1] = pack_bf16(p[2], p[3]);

@@ -1,13 +1,15 @@
 #!/bin/bash
-# fused dQ finalise v3 (16384-element tasks, mode policy): tests + A/B against K4
+# packed-fp32 (FFMA2/FADD2/FMUL2) softmax: GPU tests + A/B against the previous commit's library
 cd "$GRAFT_REPO_ROOT"
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_fused_dq.py tests/test_gpu_chunk.py -x -q > gpurun_out/at_fused_tests.txt 2>&1 || exit 1
-timeout 900 python scripts/ab_points.py fz --fused 2,0 --total --rounds 3 --scheds auto --d 64 > gpurun_out/at_points_c64.json 2>&1
-timeout 900 python scripts/ab_points.py fz --fused 2,0 --total --rounds 3 --scheds auto --d 64 --masks full > gpurun_out/at_points_f64.json 2>&1
-timeout 900 python scripts/ab_points.py fz --fused 2,0 --total --rounds 3 --scheds auto > gpurun_out/at_points_c128.json 2>&1
-for rep in 1 2 3; do
-FUSED=0 timeout 600 python scripts/ab_split.py k4 >> gpurun_out/at_split.txt 2>&1
-FUSED=1 timeout 600 python scripts/ab_split.py policy >> gpurun_out/at_split.txt 2>&1
-FUSED=2 timeout 600 python scripts/ab_split.py fused >> gpurun_out/at_split.txt 2>&1
+V=paper_2601_21824_b200/variants/libdash_head.so
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/au_tests.txt 2>&1 || exit 1
+for rep in 1 2; do
+for lib in new head; do
+  if [ $lib = head ]; then export DASH_LIB_PATH=$V; else unset DASH_LIB_PATH; fi
+  timeout 900 python scripts/ab_points.py $lib --rounds 1 --reps 20 --d 64 --masks causal,full >> gpurun_out/au_points_d64.txt 2>&1
+  timeout 900 python scripts/ab_points.py $lib --rounds 1 --reps 20 --masks causal,full >> gpurun_out/au_points_d128.txt 2>&1
+  timeout 600 python scripts/ab_split.py $lib >> gpurun_out/au_split.txt 2>&1
 done
+done
+unset DASH_LIB_PATH
