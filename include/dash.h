@@ -14,7 +14,8 @@
  *    Algorithm 1's "Q, K, V, O, dO in R^{N x d}, logsumexp L in R^N"
  *    for every (batch, head).
  *  - Supported: d in {64, 128}; N a positive multiple of 128 (the KV/Q tile
- *    size B_r = B_c = 128 of the schedule model, AMB-11); seqlen_q = seqlen_k.
+ *    size B_r = B_c = 128 of the schedule model, AMB-11); seqlen_q = seqlen_k;
+ *    B * N * H < 2^31 rows.
  *  - softmax_scale <= 0 selects 1/sqrt(d) (AMB-1).
  *  - Device pointers are CUDA device pointers owned by the caller.  All
  *    scratch lives in the caller-provided workspace; the only device memory

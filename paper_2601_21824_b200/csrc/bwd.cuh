@@ -1036,6 +1036,27 @@ __global__ void __launch_bounds__(512, 1)
   if (tid == 0 && ptx::aborted()) atomicExch(args.error_flag, 2);
 }
 
+// floor(n / d) for 0 <= n < 2^31 by one 64-bit multiply and shift (d fixed per
+// launch): m = ceil(2^s / d) with s = 32 + ceil(log2 d) is exact on that range.
+// The preprocess / convert kernels spend most of their issue slots on the
+// (b, n, h) <-> (b, h, n) index maps otherwise (64-bit divisions).
+struct FastDiv {
+  uint64_t m;
+  uint32_t s, d;
+  __host__ static FastDiv make(uint32_t d) {
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    FastDiv f;
+    f.s = 32 + l;
+    f.m = ((1ull << f.s) + d - 1) / d;
+    f.d = d;
+    return f;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return static_cast<uint32_t>((static_cast<uint64_t>(n) * m) >> s);
+  }
+};
+
 // K1: D = rowsum(dO o O) (Alg.1 line 1; D in R^N per AMB-2), fp32 in a
 // fixed order, and lse2 = -L * log2(e) for the exp2 form of P = exp(S - L);
 // also resets tickets / job counter / error flag and (atomic variant only)
@@ -1048,8 +1069,8 @@ template <int D>
 __global__ void __launch_bounds__(256) dash_preprocess_kernel(
     const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
     const float* __restrict__ lse, float* __restrict__ Dvec, float* __restrict__ lse2, int B, int N,
-    int H, int* __restrict__ zero_i32, int n_zero_i32, float4* __restrict__ zero_f32,
-    size_t n_zero_f4, int* __restrict__ counters, int poison) {
+    int H, FastDiv fN, FastDiv fH, int* __restrict__ zero_i32, int n_zero_i32,
+    float4* __restrict__ zero_f32, size_t n_zero_f4, int* __restrict__ counters, int poison) {
   constexpr int T = D / 8;      // threads per row, 16 B each
   constexpr int RPB = 256 / T;  // rows per block and half-iteration
   ptx::griddep_wait();    // the previous call's kernels may still read this workspace
@@ -1058,8 +1079,9 @@ __global__ void __launch_bounds__(256) dash_preprocess_kernel(
   const int part = static_cast<int>(threadIdx.x % T);
   auto row_addr = [&](size_t r) { return r * D + part * 8; };  // r = (b*N + n)*H + h
   auto vec_idx = [&](size_t r) {  // -> (b*H + h)*N + n, the index of D / lse2 / L
-    const size_t bn = r / H;
-    return (bn / N * H + r % H) * N + bn % N;
+    const uint32_t r32 = static_cast<uint32_t>(r);  // rows < 2^31 (dash_api.cu)
+    const uint32_t bn = fH.div(r32), b = fN.div(bn);
+    return (static_cast<size_t>(b) * H + (r32 - bn * H)) * N + (bn - b * N);
   };
   auto dot = [](uint4 a, uint4 c) {
     const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
@@ -1129,8 +1151,8 @@ __global__ void __launch_bounds__(256) dash_preprocess_kernel(
 // one-wave grid-stride grid).
 template <int D, int W>
 __global__ void __launch_bounds__(256) dash_dq_convert_kernel(
-    const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq, int N, int H, float scale,
-    int causal, int tile, int bh_base, int bh_count) {
+    const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq, int N, int H, FastDiv fN,
+    FastDiv fH, float scale, int causal, int tile, int bh_base, int bh_count) {
   constexpr int T = D / 8;
   ptx::griddep_wait();  // every ordered add of the main kernel has landed
   ptx::griddep_launch();
@@ -1146,8 +1168,8 @@ __global__ void __launch_bounds__(256) dash_dq_convert_kernel(
       const size_t i = i0 + u * stride;
       planes[u] = 0;
       if (i < total) {
-        const size_t r = i / T;  // (local head)*N + n
-        const int n = static_cast<int>(r % N);
+        const uint32_t r = static_cast<uint32_t>(i / T);  // (local head)*N + n
+        const int n = static_cast<int>(r - fN.div(r) * N);
         const int cnt = causal ? n / tile + 1 : N / tile;  // contributions to this row's Q tile
         planes[u] = W < cnt ? W : cnt;  // accumulator w holds ranks w, w + W, ...
         const float* src = acc + r * D + (i % T) * 8;
@@ -1174,11 +1196,12 @@ __global__ void __launch_bounds__(256) dash_dq_convert_kernel(
                            s1.w + x[u][w][1].w);
         }
       }
-      const size_t r = i / T;
-      const int n = static_cast<int>(r % N);
-      const size_t bh = bh_base + r / N;
-      const int h = static_cast<int>(bh % H);
-      const int b = static_cast<int>(bh / H);
+      const uint32_t r = static_cast<uint32_t>(i / T);
+      const uint32_t lh = fN.div(r);
+      const int n = static_cast<int>(r - lh * N);
+      const uint32_t bh = bh_base + lh;
+      const int b = static_cast<int>(fH.div(bh));
+      const int h = static_cast<int>(bh - b * H);
       uint4 out;
       out.x = pack_bf16(s0.x * scale, s0.y * scale);
       out.y = pack_bf16(s0.z * scale, s0.w * scale);

@@ -134,6 +134,8 @@ bool shape_ok(const dash_shape* s) {
   if (s->batch < 1 || s->heads < 1 || s->seqlen < 128 || s->seqlen % 128) return false;
   if (s->head_dim != 64 && s->head_dim != 128) return false;
   if (s->seqlen / 128 > 32767) return false;
+  // rows B*N*H index 32-bit maps in K1 / K4 (FastDiv)
+  if (static_cast<int64_t>(s->batch) * s->seqlen * s->heads >= (int64_t(1) << 31)) return false;
   return true;
 }
 bool aligned16(const void* p) { return p && (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -461,8 +463,8 @@ void launch_preprocess(const dash_shape* s, const void* o, const void* dout, con
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, dash_preprocess_kernel<D>, static_cast<const __nv_bfloat16*>(o),
                      static_cast<const __nv_bfloat16*>(dout), lse, dvec, lse2, s->batch, s->seqlen,
-                     s->heads, tickets, n_tickets, reinterpret_cast<float4*>(zero), n_zero_f4,
-                     counters, poison);
+                     s->heads, FastDiv::make(s->seqlen), FastDiv::make(s->heads), tickets, n_tickets,
+                     reinterpret_cast<float4*>(zero), n_zero_f4, counters, poison);
 }
 template <int D>
 void launch_convert(const dash_shape* s, const float* dqacc, void* dq, int W, int causal, int tile,
@@ -485,7 +487,8 @@ void launch_convert(const dash_shape* s, const float* dqacc, void* dq, int W, in
               : W == 2 ? dash_dq_convert_kernel<D, 2>
               : W == 4 ? dash_dq_convert_kernel<D, 4>
                        : dash_dq_convert_kernel<D, 8>;
-  cudaLaunchKernelEx(&cfg, kern, dqacc, out, s->seqlen, s->heads, sc, c, tile, bh_base, bh_count);
+  cudaLaunchKernelEx(&cfg, kern, dqacc, out, s->seqlen, s->heads, FastDiv::make(s->seqlen),
+                     FastDiv::make(s->heads), sc, c, tile, bh_base, bh_count);
 }
 
 template <int D>
