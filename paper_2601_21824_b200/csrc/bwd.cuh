@@ -1065,7 +1065,7 @@ struct FastDiv {
 // faster than (b, h, n) order, whose 256-B rows lie 4 KB apart), T = d / 8
 // threads per row with 16 B streaming loads each, two rows per thread and
 // iteration (four loads in flight), grid-stride over a one-wave grid.
-template <int D>
+template <int D, int KR>
 __global__ void __launch_bounds__(256) dash_preprocess_kernel(
     const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
     const float* __restrict__ lse, float* __restrict__ Dvec, float* __restrict__ lse2, int B, int N,
@@ -1096,34 +1096,27 @@ __global__ void __launch_bounds__(256) dash_preprocess_kernel(
     }
     return acc;
   };
-  for (size_t base = static_cast<size_t>(blockIdx.x) * 2 * RPB; base < rows;
-       base += static_cast<size_t>(gridDim.x) * 2 * RPB) {
-    const size_t r0 = base + threadIdx.x / T, r1 = r0 + RPB;
-    const bool v0 = r0 < rows, v1 = r1 < rows;
-    uint4 a0 = make_uint4(0, 0, 0, 0), c0 = a0, a1 = a0, c1 = a0;
-    if (v0) {
-      a0 = __ldcs(reinterpret_cast<const uint4*>(o + row_addr(r0)));
-      c0 = __ldcs(reinterpret_cast<const uint4*>(dout + row_addr(r0)));
-    }
-    if (v1) {
-      a1 = __ldcs(reinterpret_cast<const uint4*>(o + row_addr(r1)));
-      c1 = __ldcs(reinterpret_cast<const uint4*>(dout + row_addr(r1)));
-    }
-    float s0 = dot(a0, c0), s1 = dot(a1, c1);
+  for (size_t base = static_cast<size_t>(blockIdx.x) * KR * RPB; base < rows;
+       base += static_cast<size_t>(gridDim.x) * KR * RPB) {
+    uint4 av[KR], cv[KR];
 #pragma unroll
-    for (int m = T / 2; m >= 1; m >>= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, m);
-      s1 += __shfl_xor_sync(0xffffffffu, s1, m);
-    }
-    if (part == 0) {
-      if (v0) {
-        const size_t i = vec_idx(r0);
-        Dvec[i] = s0;
-        lse2[i] = -lse[i] * 1.4426950408889634f;
+    for (int u = 0; u < KR; ++u) {  // every row's loads in flight together
+      const size_t r = base + threadIdx.x / T + u * RPB;
+      av[u] = cv[u] = make_uint4(0, 0, 0, 0);
+      if (r < rows) {
+        av[u] = __ldcs(reinterpret_cast<const uint4*>(o + row_addr(r)));
+        cv[u] = __ldcs(reinterpret_cast<const uint4*>(dout + row_addr(r)));
       }
-      if (v1) {
-        const size_t i = vec_idx(r1);
-        Dvec[i] = s1;
+    }
+#pragma unroll
+    for (int u = 0; u < KR; ++u) {
+      const size_t r = base + threadIdx.x / T + u * RPB;
+      float sd = dot(av[u], cv[u]);
+#pragma unroll
+      for (int m = T / 2; m >= 1; m >>= 1) sd += __shfl_xor_sync(0xffffffffu, sd, m);
+      if (part == 0 && r < rows) {
+        const size_t i = vec_idx(r);
+        Dvec[i] = sd;
         lse2[i] = -lse[i] * 1.4426950408889634f;
       }
     }

@@ -450,8 +450,9 @@ void launch_preprocess(const dash_shape* s, const void* o, const void* dout, con
                        float* dvec, float* lse2, int* tickets, int n_tickets, float* zero,
                        size_t n_zero_f4, int* counters, int poison, int sms, cudaStream_t stream) {
   constexpr int RPB = 256 / (D / 8);
+  constexpr int kr = 2;  // rows per thread and iteration (4 measured 7 % slower)
   const size_t rows = static_cast<size_t>(s->batch) * s->seqlen * s->heads;
-  size_t g = (rows + 2 * RPB - 1) / (2 * RPB);
+  size_t g = (rows + kr * RPB - 1) / (kr * RPB);
   if (g > static_cast<size_t>(sms) * 8) g = static_cast<size_t>(sms) * 8;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(g));
@@ -461,7 +462,7 @@ void launch_preprocess(const dash_shape* s, const void* o, const void* dout, con
   set_pdl(&attr[0]);
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, dash_preprocess_kernel<D>, static_cast<const __nv_bfloat16*>(o),
+  cudaLaunchKernelEx(&cfg, dash_preprocess_kernel<D, kr>, static_cast<const __nv_bfloat16*>(o),
                      static_cast<const __nv_bfloat16*>(dout), lse, dvec, lse2, s->batch, s->seqlen,
                      s->heads, FastDiv::make(s->seqlen), FastDiv::make(s->heads), tickets, n_tickets,
                      reinterpret_cast<float4*>(zero), n_zero_f4, counters, poison);
