@@ -536,6 +536,8 @@ def main():
     ap.add_argument("--full", action="store_true", help="full mask instead of causal")
     ap.add_argument("--schedule", default=None,
                     help="naive | descending | shift | auto (default: auto, the library's per-shape choice)")
+    ap.add_argument("--fused-dq", type=int, default=None, choices=[0, 1, 2],
+                    help="dash_attn_bwd_set_fused_dq: 0 = K4 convert kernel, 1 = library policy (default), 2 = always in-kernel")
     ap.add_argument("--acc-split", type=int, default=None,
                     help="interleaved dQ accumulators W in {1,2,4,8} (AMB-27); default: the library's automatic choice")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
@@ -568,6 +570,8 @@ def main():
     import torch
     world, rank, local = dist_setup(args)
     from paper_2601_21824_b200 import dash
+    if args.fused_dq is not None:
+        dash.set_fused_dq(args.fused_dq)
     if args.acc_split is not None:
         dash.set_acc_split(args.acc_split)
     args.acc_split = dash.acc_split()  # 0 = automatic (per seqlen: sweep rows)
