@@ -430,12 +430,15 @@ cudaError_t reset_chunk(char* ws, const WsLayout& w, int deterministic, cudaStre
 
 // Programmatic dependent launch between the call's kernels (K1 -> K2 -> K4):
 // each kernel waits (griddepcontrol.wait) before touching what its
-// predecessor writes, so its launch and prologue overlap the predecessor's
-// tail.  DASH_PDL=0 turns the attribute off (experiments).
+// predecessor writes, so its launch and prologue can overlap the
+// predecessor's tail.  Off by default: measured back to back with nothing
+// between the kernels it is 2-2.5 % slower per step (with CUDA events recorded
+// between the kernels, as in the first measurement, it is inert;
+// profiles/r02_experiments_pdl.txt).  DASH_PDL=1 turns it on (experiments).
 bool pdl_on() {
   static const bool on = [] {
     const char* e = std::getenv("DASH_PDL");
-    return !(e && std::atoi(e) == 0);
+    return e && std::atoi(e) == 1;
   }();
   return on;
 }
