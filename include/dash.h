@@ -110,16 +110,18 @@ size_t dash_attn_bwd_workspace_bytes(const dash_shape* shape, int causal, int sc
  *    results are bitwise identical run to run and across (b, h) sharding.
  *  deterministic == 0: the atomic comparison variant (Fig.1) -- the
  *    same kernel with unordered reduce-adds; Q order still follows `schedule`.
- * dq, dk, dv are written (not accumulated); dq = bf16(scale * accumulator)
- * by a convert kernel after the main kernel.  o and lse must come from the
+ * dq, dk, dv are written (not accumulated); dq = bf16(scale * accumulator),
+ * formed in the main kernel's tail or by a convert kernel after it (see
+ * dash_attn_bwd_set_fused_dq).  o and lse must come from the
  * forward of the same inputs (dash_attn_fwd or any exact equivalent).
  * SHIFT with causal and an odd number of KV tiles runs the Symmetric Shift of
  * n_kv + 1 tiles without the phantom tile (DESIGN.md AMB-29).
  * SHIFT with the full mask and n_kv > 128 runs in groups of <= 128 KV tiles
- * (AMB-30).
+ * (AMB-30); SHIFT causal with more than 128 tile pairs in groups of <= 128
+ * pairs (AMB-35).
  * DASH_ERR_UNSUPPORTED: SHIFT needing more co-resident CTAs than the device
- * holds (min(n_kv, 128-tile group) for full, ceil(n_kv/2) for causal; App. B of
- * SURVEY.md, AMB-12).
+ * holds (one group: min(n_kv, 128) for full, min(ceil(n_kv/2), 128) for
+ * causal; App. B of SURVEY.md, AMB-12).
  * DASH_ERR_WORKSPACE: workspace_bytes < dash_attn_bwd_workspace_bytes(). */
 dash_status dash_attn_bwd(const dash_shape* shape, const void* q, const void* k, const void* v,
                           const void* o, const void* dout, const float* lse,

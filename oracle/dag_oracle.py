@@ -63,7 +63,7 @@ class Job:
     steps: list | None = None
 
 
-SHIFT_GROUP = 128  # AMB-30: largest group of KV tiles in one cyclic shift
+SHIFT_GROUP = 128  # AMB-30 / AMB-35: largest group of KV tiles (full) / pairs (causal) in one shift
 
 
 def task_exists(i: int, j: int, mask: int) -> bool:
@@ -95,10 +95,16 @@ def build_jobs(schedule: int, n: int, mask: int) -> list[Job]:
         # phantom KV tile n and the phantom Q tile n: every real task keeps the
         # visit step it has there, so each dQ_j keeps its step order.
         for job in build_jobs(SHIFT, n + 1, CAUSAL):
-            kept = [(t, (i, j)) for t, (i, j) in enumerate(job.tasks) if i < n and j < n]
+            steps = job.steps if job.steps is not None else range(len(job.tasks))
+            kept = [(t, (i, j)) for t, (i, j) in zip(steps, job.tasks) if i < n and j < n]
             jobs.append(Job([ij for _, ij in kept], [t for t, _ in kept]))
     elif schedule == SHIFT and mask == CAUSAL:
         h = n // 2
+        # AMB-35: more than SHIFT_GROUP pairs -> G = ceil(h / SHIFT_GROUP)
+        # consecutive near-equal groups of pairs; the jobs are unchanged, dQ_j
+        # takes group 0's contributions first, then group 1's, ..., each group
+        # in visit-step order: the step label (group, t) carries that order.
+        G = -(-h // SHIFT_GROUP)
         for p in range(h):
             tasks = []
             # Phase 1: cyclic shift over the dense lower-left rectangle,
@@ -111,7 +117,8 @@ def build_jobs(schedule: int, n: int, mask: int) -> list[Job]:
             # Phase 2, right (lower) triangle: column n-1-p, bottom-up to the diagonal.
             for j in range(n - 1, n - 2 - p, -1):
                 tasks.append((n - 1 - p, j))
-            jobs.append(Job(tasks))
+            g = next(g for g in range(G) if g * h // G <= p < (g + 1) * h // G)
+            jobs.append(Job(tasks, [(g, t) for t in range(len(tasks))] if G > 1 else None))
     else:
         raise ValueError(f"unknown schedule {schedule}")
     return jobs

@@ -8,7 +8,8 @@
 //   j >= h, i <  h : (j - h - i) mod h      (phase 1, cyclic rectangle)
 //   j >= h, i >= h : i                      (phase 2, right triangle)
 //   j <  h         : j - i                  (phase 2, left triangle)
-// Odd n: the n + 1 schedule without the phantom tile n (AMB-29).
+// Odd n: the n + 1 schedule without the phantom tile n (AMB-29).  More than
+// kShiftGroup KV tiles (full) / pairs (causal): groups, AMB-30 / AMB-35.
 #include "schedule.h"
 
 #include <algorithm>
@@ -78,28 +79,60 @@ bool build_schedule(int schedule, int n, int mask, ScheduleTable* out) {
         if (e.tasks[k].kv < n && e.tasks[k].q < n) t.tasks.push_back(e.tasks[k]);
     }
   } else if (schedule == kShift && mask == kCausal) {
+    // Pairs p = (KV p, KV n-1-p), h = n/2 of them.  More than kShiftGroup pairs
+    // (AMB-35): G = ceil(h / kShiftGroup) consecutive near-equal groups of
+    // pairs [lo, hi); the jobs are the paper's, dQ_j takes group 0's
+    // contributions first, then group 1's, ..., each group in visit-step order
+    // (G = 1: the paper's Symmetric Shift, ranks as in the header comment).
+    // Per group, for Q tile j (a = j - h, r = n - 1 - j):
+    //   rectangle, KV p -> j >= h (step (a - p) mod h):
+    //     lo + max(0, lo - r) + #{q in [lo, hi): (a - q) mod h < (a - p) mod h}
+    //   right triangle, KV n-1-p -> j >= n-1-p (steps after the rectangle,
+    //     ascending KV):  lo + max(0, lo - r) + (hi - lo) + (hi - 1 - p)
+    //   left triangle, KV p -> j < h, p <= j (KV descending):
+    //     min(lo, j + 1) + min(hi - 1, j) - p
     const int h = n / 2;
+    const int G = (h + kShiftGroup - 1) / kShiftGroup;
     t.jobs = h;
-    t.coresident = h;
-    for (int p = 0; p < h; ++p) {
-      push_job();
-      for (int s = 0; s <= n; ++s) {
-        int i, j;
-        if (s < h) {
-          i = p;
-          j = h + (p + s) % h;
-        } else if (s < n - p) {
-          i = p;
-          j = p + (s - h);
-        } else {
-          i = n - 1 - p;
-          j = (n - 1) - (s - (n - p));
+    for (int g = 0; g < G; ++g) {
+      const int lo = static_cast<int>(static_cast<int64_t>(g) * h / G);
+      const int hi = static_cast<int>(static_cast<int64_t>(g + 1) * h / G);
+      const int gs = hi - lo;
+      t.coresident = std::max(t.coresident, gs);
+      // position of KV p's rectangle step among the group's steps for Q j:
+      // the steps (a - q) mod h, q = hi-1 .. lo, are the cyclic range that
+      // starts at (a - hi + 1) mod h; if it wraps past h - 1, the w smallest
+      // values 0 .. w-1 (q = lo .. lo+w-1) come first
+      auto rect_pos = [&](int a, int p) {
+        const int start = pos_mod(a - hi + 1, h);
+        const int u = pos_mod(a - p, h);
+        const int w = start + gs - h;  // > 0 iff the range wraps
+        if (w > 0 && u < w) return u;
+        return (hi - 1 - p) + (w > 0 ? w : 0);
+      };
+      for (int p = lo; p < hi; ++p) {
+        push_job();
+        for (int s = 0; s <= n; ++s) {
+          int i, j;
+          if (s < h) {
+            i = p;
+            j = h + (p + s) % h;
+          } else if (s < n - p) {
+            i = p;
+            j = p + (s - h);
+          } else {
+            i = n - 1 - p;
+            j = (n - 1) - (s - (n - p));
+          }
+          int rank;
+          if (j >= h) {
+            const int base = lo + std::max(0, lo - (n - 1 - j));
+            rank = (i < h) ? base + rect_pos(j - h, p) : base + gs + (hi - 1 - p);
+          } else {
+            rank = std::min(lo, j + 1) + std::min(hi - 1, j) - p;
+          }
+          t.tasks.push_back({i, j, rank});
         }
-        int rank;
-        if (j >= h && i < h) rank = pos_mod(j - h - i, h);
-        else if (j >= h) rank = i;
-        else rank = j - i;
-        t.tasks.push_back({i, j, rank});
       }
     }
   } else {

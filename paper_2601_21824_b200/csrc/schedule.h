@@ -29,8 +29,9 @@ struct ScheduleTable {
 };
 
 // SHIFT full with more than kShiftGroup KV tiles runs in groups of at most
-// kShiftGroup tiles (AMB-30): a fixed constant, so tables never depend on the
-// device.
+// kShiftGroup tiles (AMB-30), SHIFT causal with more than kShiftGroup pairs
+// in groups of at most kShiftGroup pairs (AMB-35): a fixed constant, so
+// tables never depend on the device.
 constexpr int kShiftGroup = 128;
 
 // Returns false (and leaves *out empty) for an unsupported combination.

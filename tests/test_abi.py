@@ -51,7 +51,8 @@ def test_status_strings_and_version(dash):
 @pytest.mark.parametrize("mask", [dag.FULL, dag.CAUSAL])
 def test_schedule_table_matches_oracle(dash, schedule, mask):
     """The product's closed-form tables equal the oracle's definition-driven ones."""
-    for n in list(range(1, 70)) + [129, 257]:  # + grouped SHIFT full (AMB-30)
+    # + grouped SHIFT full (AMB-30: 129, 257) and causal (AMB-35: 257, 258, 301, 512, 513)
+    for n in list(range(1, 70)) + [129, 256, 257, 258, 301, 512, 513]:
         jobs = dash.schedule_table(schedule, n, mask)
         ojobs = dag.build_jobs(schedule, n, mask)
         ranks = dag.reduction_ranks(schedule, n, mask)
@@ -81,6 +82,20 @@ def test_critical_path_matches_oracle_simulator(dash):
                             assert got == want, (schedule, mask, n, m, c, r, n_sm)
                             checked += 1
     assert checked > 2000
+
+
+def test_critical_path_grouped_shift_matches_oracle(dash):
+    """Grouped SHIFT (AMB-30 full, AMB-35 causal): the product's DAG model equals
+    the oracle simulator on one group's worth of SMs and on the whole device."""
+    for mask, n in ((dag.CAUSAL, 258), (dag.CAUSAL, 301), (dag.FULL, 257)):
+        for n_sm in (65, 129, 148):
+            try:
+                want = dag.simulate(dag.SHIFT, n, mask, 1, n_sm, 3, 1)
+            except dag.Deadlock:
+                with pytest.raises(dash.DashError):
+                    dash.schedule_critical_path(dash.SHIFT, n, n, mask, 1, n_sm, 3, 1)
+                continue
+            assert dash.schedule_critical_path(dash.SHIFT, n, n, mask, 1, n_sm, 3, 1) == want
 
 
 def test_critical_path_defaults_and_errors(dash):

@@ -323,6 +323,30 @@ def test_grouped_shift_full_mask_32k(dash):
     assert np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-30) <= GRAD_TOL
 
 
+def test_grouped_symmetric_shift_pair_kernel(dash):
+    """AMB-35 on the CTA-pair kernel: causal SHIFT at N = 66048 (258 KV tiles of
+    256 rows = 129 pairs > one 128-pair group; two groups of 64 / 65 pairs fit
+    the 74 co-resident CTA pairs): sampled dQ rows against the fp64 oracle,
+    dK/dV against NAIVE within tolerance, bitwise repeatable."""
+    B, N, H, d = 1, 66048, 1, 128
+    assert dash.tile((B, N, H, d), True, "shift") == 256
+    cpu, g = _inputs(B, N, H, d, seed=4)
+    o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], True)
+    r1 = dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, True, "shift", True)
+    r2 = dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, True, "shift", True)
+    rn = dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, True, "naive", True)
+    torch.cuda.synchronize()
+    for a, b in zip(r1, r2):
+        assert torch.equal(a, b)
+    for a, b in zip(r1, rn):
+        assert (a.float() - b.float()).abs().max().item() <= 1e-2 * b.float().abs().max().item()
+    f = {k: v.double().numpy() for k, v in cpu.items()}
+    rows = [0, 257, 33023, 33024, 66047]
+    ref = oracle.attn_bwd_dq_rows(f["q"], f["k"], f["v"], f["do"], True, [0], rows)
+    got = np.stack([r1[0][0, rows, 0].float().cpu().numpy()]).astype(np.float64)
+    assert np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-30) <= GRAD_TOL
+
+
 def test_cuda_graph_capture_replays_bitwise(dash):
     """dash_attn_bwd is stream-ordered with caller-owned memory, so after a
     warm-up call (which uploads the schedule tables) it can be captured in a

@@ -165,3 +165,14 @@ def test_replay_both_kernels_d128(dash, tile, W, causal, schedule):
     finally:
         dash.set_tile(0)
         dash.set_acc_split(old_w)
+
+
+def test_replay_grouped_symmetric_shift(dash):
+    """AMB-35: causal SHIFT with n = 258 KV tiles (129 pairs > the 128-pair
+    group) runs in two groups of 64 / 65 pairs; every dQ tile's partials,
+    re-summed group-major in visit-step order (the oracle's ranks), give the
+    GPU's accumulator and dq bits (d = 64, N = 33024, one head, W = 8)."""
+    B, N, H, d = 1, 33024, 1, 64
+    W = dash.acc_split((B, N, H, d), True, "shift")
+    per_plane = _replay(dash, W, B, N, H, d, True, "shift")
+    assert all(c >= 2 for c in per_plane[:W]), per_plane

@@ -266,3 +266,38 @@ def test_grouped_shift_full_beyond_group_size():
             assert [rank[(i, j)] for _, i in order] == list(range(n))
         # the model finishes with one group's worth of SMs (co-residency of a group)
         assert dag.simulate(SHIFT, n, FULL, 1, max(sizes.values()), 2, 1) > 0
+
+
+@pytest.mark.parametrize("n", [258, 301, 400])
+def test_grouped_symmetric_shift_beyond_group_size(n):
+    """AMB-35: causal SHIFT with more than SHIFT_GROUP pairs keeps the paper's
+    jobs (pair p = KV p then KV n-1-p) and reduces each dQ_j
+    group-major, in visit-step order inside a group: every causal task exactly
+    once, conflict-free steps inside a group, each dQ_j's ranks 0..j with all
+    of group g's contributions before group g+1's, and the DAG model finishes
+    on one group's worth of SMs (co-residency of a group, not of all pairs)."""
+    jobs = dag.build_jobs(SHIFT, n, CAUSAL)
+    rank = dag.reduction_ranks(SHIFT, n, CAUSAL)
+    h = (n + 1) // 2
+    G = -(-h // dag.SHIFT_GROUP)
+    assert G >= 2 and len(jobs) == h
+    seen = [(i, j) for job in jobs for (i, j) in job.tasks]
+    assert sorted(seen) == [(i, j) for i in range(n) for j in range(i, n)]
+    sizes = {}
+    for job in jobs:
+        sizes[job.steps[0][0]] = sizes.get(job.steps[0][0], 0) + 1
+    assert len(sizes) == G and max(sizes.values()) <= dag.SHIFT_GROUP
+    assert max(sizes.values()) - min(sizes.values()) <= 1
+    by_label = {}
+    for job in jobs:
+        for lab, (i, j) in zip(job.steps, job.tasks):
+            by_label.setdefault(lab, []).append(j)
+    assert all(len(set(js)) == len(js) for js in by_label.values())
+    for j in (0, 1, h - 1, h, n // 2 + 3, n - 2, n - 1):
+        contrib = sorted((rank[(i, j)], lab[0], lab) for job in jobs
+                         for lab, (i, jj) in zip(job.steps, job.tasks) if jj == j)
+        assert [r for r, _, _ in contrib] == list(range(j + 1))
+        groups = [g for _, g, _ in contrib]
+        assert groups == sorted(groups)                 # group-major
+        assert [lab for _, _, lab in contrib] == sorted(lab for _, _, lab in contrib)
+    assert dag.simulate(SHIFT, n, CAUSAL, 1, max(sizes.values()), 2, 1) > 0
