@@ -69,6 +69,8 @@ def test_fused_mode_default_and_launch_count(dash):
     (1, 4096, 2, 128, 256, False, "shift", 8),      # pair, W = 8 (every plane live at n = 16)
     (1, 2048, 8, 128, 256, True, "naive", 1),
     (8, 512, 8, 64, 0, True, "shift", 0),           # d = 64
+    (3, 384, 2, 64, 0, True, "shift", 0),           # d = 64, ragged last finalise task (256 rows)
+    (2, 128, 3, 64, 0, False, "naive", 0),          # one KV tile, one partial task
     (1, 4096, 4, 64, 0, False, "descending", 4),
     (1, 8192, 2, 64, 0, True, "descending", 8),
 ])
