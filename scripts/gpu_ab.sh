@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B of the working tree's libdash.so against paper_2601_21824_b200/variants/libdash_head.so
-# (the previous commit, built by hand): selected GPU tests, then interleaved per-point and
+# (python scripts/build_variant.py head --rev HEAD): selected GPU tests, then interleaved per-point and
 # whole-step timings.   gpurun -- 'bash scripts/gpu_ab.sh TAG "pytest -k args"'
 T=${1:-ab}
 cd "$GRAFT_REPO_ROOT"
