@@ -536,6 +536,8 @@ def main():
     ap.add_argument("--full", action="store_true", help="full mask instead of causal")
     ap.add_argument("--schedule", default=None,
                     help="naive | descending | shift | auto (default: auto, the library's per-shape choice)")
+    ap.add_argument("--graph", action="store_true",
+                    help="time the step as one CUDA graph replay (captured after warm-up)")
     ap.add_argument("--fused-dq", type=int, default=None, choices=[0, 1, 2],
                     help="dash_attn_bwd_set_fused_dq: 0 = K4 convert kernel, 1 = library policy (default), 2 = always in-kernel")
     ap.add_argument("--acc-split", type=int, default=None,
@@ -593,9 +595,21 @@ def main():
     rank_tile = sum(tile_flops(*g["shape"], causal) for _, g in probs)
 
     # --- headline: device-timed sweep step -----------------------------------
+    # --graph: the step (every sweep point's dash_attn_bwd) captured once in a
+    # CUDA graph and replayed -- the library is stream-ordered and
+    # allocation-free, so the replay runs the same kernels on the same buffers.
+    timed_step = step
+    if args.graph:
+        for _ in range(max(1, args.warmup)):
+            step()  # schedule tables uploaded before capture
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        timed_step = graph.replay
     with ClockSampler(local) as clk:
         time.sleep(0.3)  # let nvidia-smi start sampling before the timed region
-        ms = time_steps(torch, step, args.steps, args.warmup, world,
+        ms = time_steps(torch, timed_step, args.steps, args.warmup, world,
                         lambda: clk.mark("t0"), lambda: clk.mark("t1"))
     ms_max = max_over_ranks(ms, world)
     value = job_flops * args.steps / (ms_max / 1e3) / 1e12
