@@ -404,11 +404,12 @@ def test_long_context_config4_sampled_rows(dash):
             assert np.max(np.abs(x - r)) / np.max(np.abs(r)) <= GRAD_TOL
 
 
-@pytest.mark.parametrize("schedule,causal,N", [
-    ("descending", True, 8192),   # W = 4 and early claim of the next job (prefetch on)
-    ("shift", False, 1024),       # cyclic waits inside a head (claim after release)
+@pytest.mark.parametrize("schedule,causal,N,fused", [
+    ("descending", True, 8192, 1),  # W = 4, early claim (prefetch on), pair kernel, fused dQ finalise
+    ("shift", False, 1024, 1),      # cyclic waits inside a head (claim after release), K4
+    ("shift", False, 1024, 2),      # the same on the single-CTA kernel with the fused finalise
 ])
-def test_watchdog_reports_deadlock_and_recovers(dash, schedule, causal, N):
+def test_watchdog_reports_deadlock_and_recovers(dash, schedule, causal, N, fused):
     """A ticket that never reaches its rank (fault injection: the first ticket
     preset to 1 << 30) must trip the bounded ticket wait, make every warp role
     leave (the kernel returns), and be reported as DASH_ERR_DEADLOCK by
@@ -417,6 +418,7 @@ def test_watchdog_reports_deadlock_and_recovers(dash, schedule, causal, N):
     B, H, d = 1, 4, 128
     _, g = _inputs(B, N, H, d, seed=8)
     o, lse = dash.attn_fwd(g["q"], g["k"], g["v"], causal)
+    dash.set_fused_dq(fused)
     ws = dash.alloc_workspace(g["q"].shape, causal, schedule, True)
     good = [t.clone() for t in dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal,
                                              schedule, True, workspace=ws)]
@@ -428,8 +430,11 @@ def test_watchdog_reports_deadlock_and_recovers(dash, schedule, causal, N):
         assert dash.check_workspace(g["q"].shape, causal, schedule, True, ws) == dash.ERR_DEADLOCK
     finally:
         dash.set_watchdog(0)
-    again = dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal, schedule, True,
-                          workspace=ws)
-    assert dash.check_workspace(g["q"].shape, causal, schedule, True, ws) == dash.OK
+    try:
+        again = dash.attn_bwd(g["q"], g["k"], g["v"], o, g["do"], lse, causal, schedule, True,
+                              workspace=ws)
+        assert dash.check_workspace(g["q"].shape, causal, schedule, True, ws) == dash.OK
+    finally:
+        dash.set_fused_dq(1)
     for a, b in zip(again, good):
         assert torch.equal(a, b)
